@@ -1,0 +1,454 @@
+// C ABI entry points (include/kvrerank_b200.h), small kernels, and the
+// layer-loop driver krr_forward.
+#include <math_constants.h>
+#include <mutex>
+#include <vector>
+#include "launchers.h"
+
+namespace krr {
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& m) { g_err = m; }
+int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+std::atomic<uint64_t>& launch_counter() { return g_launches; }
+int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(KRR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return KRR_OK;
+}
+
+int device_sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------- profiling
+struct ProfRec { cudaEvent_t a, b; int cls; double flops; };
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static double g_prof_ms[3] = {0, 0, 0};
+static uint64_t g_prof_n[3] = {0, 0, 0};
+static double g_prof_flops = 0.0;
+
+ProfScope::ProfScope(cudaStream_t s_, int cls_, double flops_)
+    : s(s_), cls(cls_), flops(flops_), on(g_prof_on) {
+  if (on) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+}
+ProfScope::~ProfScope() {
+  if (on) {
+    cudaEventRecord(e1, s);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof.push_back({e0, e1, cls, flops});
+  }
+}
+
+// ---------------------------------------------------------------- kernels
+// a1: SplitMix64 stream -> top 24 bits -> [-b, b] (hashing.py:58-80), written
+// in destination order; transpose maps reference [in,out] to device [out,in].
+template <typename T>
+__global__ void init_uniform_kernel(uint64_t seed, double bound, int64_t rows, int64_t cols,
+                                    int transpose, T* out, int64_t ld) {
+  const int64_t total = rows * cols;
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < total;
+       d += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r, c, src;
+    if (transpose) { c = d / rows; r = d - c * rows; }
+    else { r = d / cols; c = d - r * cols; }
+    src = r * cols + c;
+    uint64_t z = seed + (uint64_t)(src + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    const double u = (double)(z >> 40) / 16777215.0;
+    const double two_u = 2.0 * u;                  // exact
+    const float v = (float)(__dsub_rn(two_u, 1.0) * bound);
+    const int64_t dst = transpose ? c * ld + r : r * ld + c;
+    out[dst] = Act<T>::from(v);
+  }
+}
+
+// a5: x = E[tokens]  (model.py:352)
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const float* __restrict__ emb,
+                             int d, float* __restrict__ x) {
+  const int64_t r = blockIdx.x;
+  const float4* src = reinterpret_cast<const float4*>(emb + (int64_t)tok[r] * d);
+  float4* dst = reinterpret_cast<float4*>(x + r * d);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+}
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (threadIdx.x < 32) {
+    t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// RMSNorm x * (1/sqrt(mean(x^2)+1e-6)) * gain  (model.py:439-441)
+template <typename T>
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                               int d, T* __restrict__ out) {
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  const float* xr = x + r * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
+  ss = block_sum(ss, red);
+  const float inv = 1.0f / sqrtf(ss / (float)d + 1e-6f);
+  T* o = out + r * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = Act<T>::from((xr[i] * inv) * gain[i]);
+}
+
+// a10: score = rms(x[last])*final_gain . head  (model.py:402, reranker.py:211-212)
+__global__ void score_kernel(const float* __restrict__ x, int T_, int d,
+                             const int32_t* __restrict__ last, const float* __restrict__ fg,
+                             const float* __restrict__ head, float* __restrict__ scores) {
+  __shared__ float red[32];
+  const int b = blockIdx.x;
+  const float* xr = x + ((int64_t)b * T_ + last[b]) * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
+  ss = block_sum(ss, red);
+  const float inv = 1.0f / sqrtf(ss / (float)d + 1e-6f);
+  float dot = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dot = fmaf((xr[i] * inv) * fg[i], head[i], dot);
+  dot = block_sum(dot, red);
+  if (threadIdx.x == 0) scores[b] = dot;
+}
+
+// a13: per-segment top-k by (score desc, doc id asc) (pipeline.py:285-287).
+// Rank of candidate i = #{j : s_j > s_i or (s_j == s_i and id_j < id_i)}.
+__global__ void topk_kernel(const float* __restrict__ scores, const int32_t* __restrict__ ids,
+                            int seg_len, int k, int32_t* __restrict__ out_idx,
+                            float* __restrict__ out_score) {
+  extern __shared__ uint8_t sm[];
+  float* s = reinterpret_cast<float*>(sm);
+  int32_t* id = reinterpret_cast<int32_t*>(s + seg_len);
+  const int seg = blockIdx.x;
+  for (int i = threadIdx.x; i < seg_len; i += blockDim.x) {
+    s[i] = scores[(int64_t)seg * seg_len + i];
+    id[i] = ids[(int64_t)seg * seg_len + i];
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    out_idx[(int64_t)seg * k + i] = -1;
+    if (out_score) out_score[(int64_t)seg * k + i] = -CUDART_INF_F;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < seg_len; i += blockDim.x) {
+    const float si = s[i];
+    const int32_t ii = id[i];
+    int rank = 0;
+    for (int j = 0; j < seg_len; ++j) {
+      const float sj = s[j];
+      rank += (sj > si) || (sj == si && id[j] < ii) || (sj == si && id[j] == ii && j < i);
+    }
+    if (rank < k) {
+      out_idx[(int64_t)seg * k + rank] = i;
+      if (out_score) out_score[(int64_t)seg * k + rank] = si;
+    }
+  }
+}
+
+// codec.py:82-95 / 98-115: code * scale[kvh][c]; INT4 low nibble first, sign-extended.
+template <typename T>
+__global__ void dequant_kernel(const uint8_t* __restrict__ codes, const float* __restrict__ scales,
+                               int bits, int KVH, int D, int HD, T* __restrict__ out) {
+  const int64_t total = (int64_t)KVH * D * HD;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int code;
+    if (bits == 8) code = (int)(int8_t)codes[i];
+    else {
+      const uint8_t byte = codes[i >> 1];
+      const int nib = (i & 1) ? (byte >> 4) : (byte & 0xF);
+      code = (nib ^ 8) - 8;
+    }
+    const int h = (int)(i / ((int64_t)D * HD));
+    const int c = (int)(i % HD);
+    out[i] = Act<T>::from((float)code * scales[h * HD + c]);
+  }
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)device_sm_count() * 32;
+  return (unsigned)std::max<int64_t>(1, std::min(g, cap));
+}
+
+static int do_gemm(int backend, int act, const void* A, const void* B, int64_t M, int N, int K,
+                   const EpiParams& ep, cudaStream_t s) {
+  if (backend == KRR_GEMM_AUTO) backend = (act == KRR_F32) ? KRR_GEMM_SIMT : KRR_GEMM_TCGEN05;
+  ProfScope ps(s, 0, 2.0 * (double)M * N * K);
+  if (backend == KRR_GEMM_TCGEN05) return launch_gemm_tcgen05(act, A, B, M, N, K, ep, s);
+  return launch_gemm_simt(act, A, B, M, N, K, ep, s);
+}
+
+static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t s) {
+  if (backend == 0) backend = (act == KRR_F32) ? 2 : 1;
+  ProfScope ps(s, 1);
+  if (backend == 1) return launch_attention_mma(act, p, s);
+  return launch_attention_simt(act, p, s);
+}
+
+static int do_rmsnorm(const float* x, const float* gain, int64_t rows, int d, int act, void* out,
+                      cudaStream_t s) {
+  ProfScope ps(s, 2);
+  const int threads = d >= 1024 ? 256 : 128;
+  if (act == KRR_F32) rmsnorm_kernel<float><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, (float*)out);
+  else if (act == KRR_F16) rmsnorm_kernel<__half><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, (__half*)out);
+  else rmsnorm_kernel<__nv_bfloat16><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, (__nv_bfloat16*)out);
+  return check_launch("rmsnorm");
+}
+
+}  // namespace krr
+
+using namespace krr;
+
+extern "C" {
+
+const char* krr_last_error(void) { return g_err.c_str(); }
+const char* krr_version(void) { return "kvrerank_b200 0.1 sm_100a"; }
+uint64_t krr_launch_count(void) { return g_launches.load(); }
+
+int krr_profile_enable(int enable) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = enable != 0;
+  for (int i = 0; i < 3; ++i) { g_prof_ms[i] = 0; g_prof_n[i] = 0; }
+  g_prof_flops = 0.0;
+  for (auto& r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  g_prof.clear();
+  return KRR_OK;
+}
+
+int krr_profile_read(double* ms_out3, uint64_t* n_out3, double* gemm_flops) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    g_prof_ms[r.cls] += ms;
+    g_prof_n[r.cls] += 1;
+    if (r.cls == 0) g_prof_flops += r.flops;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  for (int i = 0; i < 3; ++i) {
+    if (ms_out3) ms_out3[i] = g_prof_ms[i];
+    if (n_out3) n_out3[i] = g_prof_n[i];
+  }
+  if (gemm_flops) *gemm_flops = g_prof_flops;
+  return KRR_OK;
+}
+
+int krr_init_uniform(uint64_t seed, double bound, int64_t rows, int64_t cols, int transpose,
+                     int out_dtype, void* out, int64_t out_ld, krr_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned g = grid_for(rows * cols, 256);
+  if (out_dtype == KRR_F32)
+    init_uniform_kernel<float><<<g, 256, 0, s>>>(seed, bound, rows, cols, transpose, (float*)out, out_ld);
+  else if (out_dtype == KRR_F16)
+    init_uniform_kernel<__half><<<g, 256, 0, s>>>(seed, bound, rows, cols, transpose, (__half*)out, out_ld);
+  else
+    init_uniform_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(seed, bound, rows, cols, transpose,
+                                                         (__nv_bfloat16*)out, out_ld);
+  return check_launch("init_uniform");
+}
+
+int krr_embed(const int32_t* tokens, const float* emb, int64_t rows, int32_t d, float* x,
+              krr_stream_t stream) {
+  KRR_REQUIRE(d % 4 == 0, KRR_ESHAPE, "model_dim must be a multiple of 4");
+  if (rows == 0) return KRR_OK;
+  ProfScope ps((cudaStream_t)stream, 2);
+  embed_kernel<<<(unsigned)rows, 128, 0, (cudaStream_t)stream>>>(tokens, emb, d, x);
+  return check_launch("embed");
+}
+
+int krr_rmsnorm(const float* x, const float* gain, int64_t rows, int32_t d, int out_dtype,
+                void* out, krr_stream_t stream) {
+  if (rows == 0) return KRR_OK;
+  return do_rmsnorm(x, gain, rows, d, out_dtype, out, (cudaStream_t)stream);
+}
+
+int krr_gemm(int backend, int act_dtype, const void* A, const void* B, int64_t M, int32_t N,
+             int32_t K, int epilogue, void* out, const krr_qkv_t* qkv, krr_stream_t stream) {
+  EpiParams ep{};
+  ep.kind = epilogue;
+  ep.M = M;
+  ep.N = N;
+  ep.out = out;
+  if (epilogue == KRR_EPI_QKV_ROPE) {
+    KRR_REQUIRE(qkv != nullptr, KRR_ECONFIG, "QKV epilogue needs krr_qkv_t");
+    ep.qkv = *qkv;
+  }
+  if (M == 0) return KRR_OK;
+  return do_gemm(backend, act_dtype, A, B, M, N, K, ep, (cudaStream_t)stream);
+}
+
+int krr_attention(int backend, int act_dtype, const void* q, int32_t n_seqs, int32_t kv_heads,
+                  int32_t group, int32_t head_dim, int32_t seq_len, int32_t prefix_len,
+                  int32_t layer, int32_t cur_layer, void* const* prefix_kv,
+                  const int32_t* prefix_valid_len, void* const* cur_kv,
+                  const uint8_t* tok_valid, void* out, krr_stream_t stream) {
+  AttnParams p{q, n_seqs, kv_heads, group, head_dim, seq_len, prefix_len, layer, cur_layer,
+               prefix_kv, prefix_valid_len, cur_kv, tok_valid, out};
+  if (n_seqs == 0) return KRR_OK;
+  return do_attention(backend, act_dtype, p, (cudaStream_t)stream);
+}
+
+int krr_score_head(const float* x, int32_t n_seqs, int32_t seq_len, int32_t d,
+                   const int32_t* last_index, const float* final_gain, const float* head,
+                   float* scores, krr_stream_t stream) {
+  if (n_seqs == 0) return KRR_OK;
+  ProfScope ps((cudaStream_t)stream, 2);
+  score_kernel<<<n_seqs, 256, 0, (cudaStream_t)stream>>>(x, seq_len, d, last_index, final_gain,
+                                                         head, scores);
+  return check_launch("score_head");
+}
+
+int krr_segmented_topk(const float* scores, const int32_t* doc_ids, int32_t n_seg,
+                       int32_t seg_len, int32_t k, int32_t* out_idx, float* out_score,
+                       krr_stream_t stream) {
+  KRR_REQUIRE(seg_len >= 0 && seg_len <= 16384, KRR_ESHAPE, "top-k segment too long");
+  KRR_REQUIRE(k >= 1, KRR_ECONFIG, "top-k needs k >= 1");
+  if (n_seg == 0) return KRR_OK;
+  const size_t smem = (size_t)seg_len * 8;
+  topk_kernel<<<n_seg, 256, smem, (cudaStream_t)stream>>>(scores, doc_ids, seg_len, k, out_idx,
+                                                          out_score);
+  return check_launch("segmented_topk");
+}
+
+int krr_dequant_kv(const uint8_t* codes, const float* scales, int32_t bits, int32_t kv_heads,
+                   int32_t doc_len, int32_t head_dim, int out_dtype, void* out,
+                   krr_stream_t stream) {
+  KRR_REQUIRE(bits == 8 || bits == 4, KRR_ECONFIG, "dequant bits must be 8 or 4");
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned g = grid_for((int64_t)kv_heads * doc_len * head_dim, 256);
+  if (out_dtype == KRR_F32)
+    dequant_kernel<float><<<g, 256, 0, s>>>(codes, scales, bits, kv_heads, doc_len, head_dim, (float*)out);
+  else if (out_dtype == KRR_F16)
+    dequant_kernel<__half><<<g, 256, 0, s>>>(codes, scales, bits, kv_heads, doc_len, head_dim, (__half*)out);
+  else
+    dequant_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(codes, scales, bits, kv_heads, doc_len, head_dim,
+                                                    (__nv_bfloat16*)out);
+  return check_launch("dequant_kv");
+}
+
+// ------------------------------------------------------------- layer loop
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int krr_workspace_bytes(const krr_model_t* m, int64_t rows, size_t* out) {
+  KRR_REQUIRE(m && out, KRR_ECONFIG, "null argument");
+  const size_t es = dtype_size(m->act_dtype);
+  const int64_t d = m->model_dim, hq = (int64_t)m->heads * m->head_dim;
+  size_t total = align256(rows * d * 4)          // x  (f32 residual stream)
+               + align256(rows * d * es)         // xn (normed activations)
+               + align256(rows * hq * es)        // q  ([unit][g*t][hd])
+               + align256(rows * hq * es)        // attention output
+               + align256(rows * 4 * d * es);    // MLP hidden
+  *out = total;
+  return KRR_OK;
+}
+
+int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, size_t ws_bytes,
+                krr_stream_t stream) {
+  KRR_REQUIRE(m && b, KRR_ECONFIG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int L = m->layers, d = m->model_dim, H = m->heads, KVH = m->kv_heads, HD = m->head_dim;
+  KRR_REQUIRE(H % KVH == 0 && H * HD == d, KRR_ECONFIG, "inconsistent model geometry");
+  const int G = H / KVH;
+  const int64_t rows = (int64_t)b->n_seqs * b->seq_len;
+  if (rows == 0) return KRR_OK;
+  KRR_REQUIRE(b->pos0 + b->seq_len <= m->max_position, KRR_ESHAPE, "positions exceed max_position");
+  KRR_REQUIRE(b->cur_kv_layers == 1 || b->cur_kv_layers == L, KRR_ECONFIG,
+              "cur_kv_layers must be 1 or layers");
+  size_t need = 0;
+  krr_workspace_bytes(m, rows, &need);
+  KRR_REQUIRE(ws_bytes >= need, KRR_ECONFIG, "workspace too small");
+  const int act = m->act_dtype;
+  const size_t es = dtype_size(act);
+  uint8_t* w = static_cast<uint8_t*>(workspace);
+  float* x = reinterpret_cast<float*>(w);          w += align256(rows * d * 4);
+  void* xn = w;                                    w += align256(rows * d * es);
+  void* qb = w;                                    w += align256(rows * (int64_t)H * HD * es);
+  void* ab = w;                                    w += align256(rows * (int64_t)H * HD * es);
+  void* hb = w;
+
+  int rc = krr_embed(b->tokens, m->token_embedding, rows, d, x, stream);
+  if (rc) return rc;
+  const int nqkv = (H + 2 * KVH) * HD;
+  const bool prefill_only = b->scores == nullptr;
+  for (int l = 0; l < L; ++l) {
+    rc = do_rmsnorm(x, m->attn_gain[l], rows, d, act, xn, s);
+    if (rc) return rc;
+    EpiParams ep{};
+    ep.kind = KRR_EPI_QKV_ROPE;
+    ep.M = rows;
+    ep.N = nqkv;
+    const int cl = b->cur_kv_layers == 1 ? 0 : l;
+    ep.qkv = krr_qkv_t{H, KVH, HD, b->seq_len, b->pos0, cl, b->seq_len,
+                       m->rope_cos, m->rope_sin, qb, b->cur_kv};
+    rc = do_gemm(m->gemm_backend, act, xn, m->wqkv[l], rows, nqkv, d, ep, s);
+    if (rc) return rc;
+    // Prefill needs only K/V from the last layer: the rest of that layer
+    // cannot influence any stored byte (model.py:365-400 dataflow).
+    if (prefill_only && l == L - 1) break;
+    AttnParams ap{qb, b->n_seqs, KVH, G, HD, b->seq_len, b->prefix_len, l, cl,
+                  b->prefix_kv, b->prefix_valid_len, b->cur_kv, b->tok_valid, ab};
+    rc = do_attention(m->attn_backend, act, ap, s);
+    if (rc) return rc;
+    EpiParams er{};
+    er.kind = KRR_EPI_RESIDUAL;
+    er.M = rows;
+    er.N = d;
+    er.out = x;
+    rc = do_gemm(m->gemm_backend, act, ab, m->wo[l], rows, d, H * HD, er, s);
+    if (rc) return rc;
+    rc = do_rmsnorm(x, m->mlp_gain[l], rows, d, act, xn, s);
+    if (rc) return rc;
+    EpiParams eg{};
+    eg.kind = KRR_EPI_GELU;
+    eg.M = rows;
+    eg.N = 4 * d;
+    eg.out = hb;
+    rc = do_gemm(m->gemm_backend, act, xn, m->w_up[l], rows, 4 * d, d, eg, s);
+    if (rc) return rc;
+    rc = do_gemm(m->gemm_backend, act, hb, m->w_down[l], rows, d, 4 * d, er, s);
+    if (rc) return rc;
+  }
+  if (b->scores) {
+    KRR_REQUIRE(b->last_index != nullptr, KRR_ECONFIG, "scores need last_index");
+    rc = krr_score_head(x, b->n_seqs, b->seq_len, d, b->last_index, m->final_gain,
+                        m->score_head, b->scores, stream);
+    if (rc) return rc;
+  }
+  return KRR_OK;
+}
+
+}  // extern "C"

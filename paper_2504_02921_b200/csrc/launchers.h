@@ -1,0 +1,35 @@
+// Internal launcher declarations shared across the .cu files.
+#pragma once
+#include "common.cuh"
+
+namespace krr {
+
+// Epilogue parameters shared by the tcgen05 and SIMT GEMMs.
+struct EpiParams {
+  int kind;      // KRR_EPI_*
+  int64_t M;
+  int N;
+  void* out;     // STORE/GELU: act [M,N]; RESIDUAL: f32 [M,N]
+  krr_qkv_t qkv; // QKV_ROPE scatter
+};
+
+int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, int N, int K,
+                        const EpiParams& ep, cudaStream_t s);
+int launch_gemm_simt(int act_dtype, const void* A, const void* B, int64_t M, int N, int K,
+                     const EpiParams& ep, cudaStream_t s);
+
+struct AttnParams {
+  const void* q;               // [units][group*seq_len][hd]
+  int n_seqs, kv_heads, group, head_dim, seq_len, prefix_len, layer, cur_layer;
+  void* const* prefix_kv;
+  const int32_t* prefix_valid_len;
+  void* const* cur_kv;
+  const uint8_t* tok_valid;
+  void* out;                   // [n_seqs*seq_len][heads*hd]
+};
+int launch_attention_mma(int act_dtype, const AttnParams& p, cudaStream_t s);
+int launch_attention_simt(int act_dtype, const AttnParams& p, cudaStream_t s);
+
+int device_sm_count();
+
+}  // namespace krr

@@ -1,0 +1,171 @@
+"""Batched device execution of the rerank hot path through the C ABI.
+
+The reference scores one pair per forward call (reranker.py:280-289) and
+re-streams every weight per pair.  Here every candidate pair's query suffix
+is stacked into one M dimension (rows = pairs x query_len) and the whole
+layer stack runs once per batch inside krr_forward (C++), with per-pair
+prefix KV read straight from pool slots.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError
+from .kvpool import KVPool
+from .model import DeviceWeights
+
+DEFAULT_WORKSPACE_BUDGET = 32 << 30  # bytes of activations per krr_forward call
+
+
+class _Workspace:
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device):
+        import torch
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = None
+            self.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_WS: dict = {}
+
+
+def _workspace(device):
+    return _WS.setdefault(str(device), _Workspace())
+
+
+def workspace_bytes(w: DeviceWeights, rows: int) -> int:
+    out = C.c_size_t()
+    _lib.check(_lib.lib().krr_workspace_bytes(C.byref(w.struct()), rows, C.byref(out)))
+    return out.value
+
+
+def rows_budget(w: DeviceWeights, budget: int = DEFAULT_WORKSPACE_BUDGET) -> int:
+    per_row = workspace_bytes(w, 1 << 16) / float(1 << 16)
+    return max(1, int(budget // per_row))
+
+
+def _ptr(t):
+    return 0 if t is None else t.data_ptr()
+
+
+def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
+                prefix_valid, prefix_ptrs, cur_ptrs, cur_kv_layers: int, last_index=None,
+                scores=None, stream=None) -> None:
+    """One krr_forward call over n sequences (all device tensors, contiguous):
+    tokens int32 [n, T], tok_valid uint8 [n, T], prefix_valid int32 [n],
+    prefix_ptrs / cur_ptrs int64 [n], last_index int32 [n], scores f32 [n]."""
+    import torch
+    n, T = tokens.shape
+    if n == 0:
+        return
+    rows = n * T
+    need = workspace_bytes(w, rows)
+    ws = _workspace(w.device).get(need, w.device)
+    b = _lib.Batch(n, T, pos0, prefix_len, cur_kv_layers, _ptr(tokens), _ptr(tok_valid),
+                   _ptr(prefix_valid), _ptr(prefix_ptrs), _ptr(cur_ptrs), _ptr(last_index),
+                   _ptr(scores))
+    if stream is None:
+        stream = torch.cuda.current_stream(w.device).cuda_stream
+    _lib.check(_lib.lib().krr_forward(C.byref(w.struct()), C.byref(b), ws.data_ptr(),
+                                      ws.numel(), stream))
+
+
+def prefill_slots(w: DeviceWeights, pool: KVPool, slots, doc_tokens, valid_len,
+                  max_rows: int | None = None) -> None:
+    """Document prefill (reranker.py:182-201) of n docs straight into pool
+    slots: positions [0, D), pad rows computed and kept, K/V written by the
+    QKV epilogue into the slot pages."""
+    import torch
+    if pool.code != w.code:
+        raise ConfigError(f"pool dtype {pool.dtype} != weights dtype {w.dtype}")
+    dev = w.device
+    D = pool.document_len
+    tok = torch.as_tensor(np.asarray(doc_tokens), device=dev).to(torch.int32).reshape(-1, D)
+    n = tok.shape[0]
+    valid = (tok != 0).to(torch.uint8)
+    slots_t = torch.as_tensor(np.asarray(slots), device=dev).to(torch.int64)
+    ptrs = pool.slot_ptrs(slots_t)
+    step = max(1, (max_rows or rows_budget(w)) // D)
+    for i in range(0, n, step):
+        j = min(n, i + step)
+        run_forward(w, tok[i:j].contiguous(), valid[i:j].contiguous(), 0, 0, None, None,
+                    ptrs[i:j].contiguous(), w.config.layers)
+    pool.set_valid_len(np.asarray(slots), np.asarray(valid_len))
+
+
+class SuffixScratch:
+    """Per-layer suffix K/V scratch ([n][1][2][KVH][Q][HD]), reused across layers."""
+
+    def __init__(self):
+        self.buf = None
+
+    def ptrs(self, w: DeviceWeights, n: int, Q: int):
+        import torch
+        cfg = w.config
+        shape = (n, 1, 2, cfg.kv_heads, Q, cfg.head_dim)
+        need = int(np.prod(shape))
+        tdt = w.wqkv[0].dtype
+        if self.buf is None or self.buf.numel() < need or self.buf.dtype != tdt:
+            self.buf = torch.empty(need, dtype=tdt, device=w.device)
+        per = need // n * self.buf.element_size()
+        return torch.arange(n, device=w.device, dtype=torch.int64) * per + self.buf.data_ptr()
+
+
+_SCRATCH: dict = {}
+
+
+def score_slots(w: DeviceWeights, pool: KVPool, slots, q_tokens, q_valid=None, last_index=None,
+                max_rows: int | None = None, out=None):
+    """Score pairs (pool slot, query tokens) on the device; returns f32 [n] on device.
+
+    slots int [n] (host or device), q_tokens int [n, Q] (host or device)."""
+    import torch
+    if pool.code != w.code:
+        raise ConfigError(f"pool dtype {pool.dtype} != weights dtype {w.dtype}")
+    dev = w.device
+    q = torch.as_tensor(q_tokens, device=dev)
+    if q.dtype != torch.int32:
+        q = q.to(torch.int32)
+    n, Q = q.shape
+    if q_valid is None:
+        q_valid = (q != 0).to(torch.uint8)
+    if last_index is None:
+        ar = torch.arange(Q, device=dev, dtype=torch.int32)
+        last_index = torch.where(q_valid.bool(), ar, torch.full_like(ar, -1)).max(dim=1).values
+        last_index = last_index.to(torch.int32)
+    slots_t = torch.as_tensor(slots, device=dev).to(torch.int64)
+    prefix_ptrs = pool.slot_ptrs(slots_t)
+    prefix_valid = pool.valid_len[slots_t]
+    scores = out if out is not None else torch.empty(n, dtype=torch.float32, device=dev)
+    step = max(1, (max_rows or rows_budget(w)) // Q)
+    scratch = _SCRATCH.setdefault(str(dev), SuffixScratch())
+    D = pool.document_len
+    for i in range(0, n, step):
+        j = min(n, i + step)
+        cur = scratch.ptrs(w, j - i, Q)
+        run_forward(w, q[i:j].contiguous(), q_valid[i:j].contiguous(), D, D,
+                    prefix_valid[i:j].contiguous(), prefix_ptrs[i:j].contiguous(), cur, 1,
+                    last_index[i:j].contiguous(), scores[i:j])
+    return scores
+
+
+def segmented_topk(scores, doc_ids, n_seg: int, seg_len: int, k: int):
+    """Per-segment top-k by (score desc, doc id asc) on the device.
+    Returns (idx int32 [n_seg, k], score f32 [n_seg, k]) device tensors."""
+    import torch
+    dev = scores.device
+    idx = torch.empty((n_seg, k), dtype=torch.int32, device=dev)
+    sc = torch.empty((n_seg, k), dtype=torch.float32, device=dev)
+    ids = torch.as_tensor(doc_ids, device=dev).to(torch.int32).contiguous()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _lib.check(_lib.lib().krr_segmented_topk(scores.contiguous().data_ptr(), ids.data_ptr(),
+                                             n_seg, seg_len, k, idx.data_ptr(), sc.data_ptr(),
+                                             stream))
+    return idx, sc

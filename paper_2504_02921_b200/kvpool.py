@@ -1,0 +1,182 @@
+"""Paged KV storage: an HBM pool plus a pinned host-DRAM tier.
+
+HBM layout (one slab, allocated once):
+
+    pool[slot][layer][K|V][kv_head][token][head_dim]   (16-bit, or f32 debug)
+
+One slot holds one document chunk's whole fixed-length cache (the static
+[doc | query] layout of reranker.py:1-16 makes every chunk the same size), so
+the page table is simply ``chunk_id -> slot``.  Kernels receive per-pair slot
+base pointers (device int64 array) and index ``layer``/``kv_head`` inside.
+The per-(layer, K|V, kv_head) page is ``D*HD`` contiguous elements, the same
+order as the reference's HRKV payload (codec.py:8-9), so HRKV import/export
+is a straight cast.
+
+HostKVTier is the stand-in for the paper's SSD tier:
+same slot layout in pinned host memory, streamed into an HBM staging pool
+with cudaMemcpyAsync on a side stream, event-gated against compute.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+from . import _lib
+from .config import ModelConfig
+from .errors import ShapeError, StoreError
+from .model import torch_dtype
+
+
+class KVPool:
+    def __init__(self, config: ModelConfig, document_len: int, capacity: int,
+                 dtype: str = "f16", device=None):
+        import torch
+        if capacity < 1:
+            raise StoreError("pool capacity must be >= 1")
+        self.config = config
+        self.document_len = document_len
+        self.capacity = capacity
+        self.dtype = dtype
+        self.code = _lib.DTYPE_CODES[dtype]
+        self.device = torch.device(device if device is not None else "cuda")
+        L, KVH, HD = config.layers, config.kv_heads, config.head_dim
+        self.page_shape = (L, 2, KVH, document_len, HD)
+        self.slab = torch.empty((capacity, *self.page_shape), dtype=torch_dtype(self.code),
+                                device=self.device)
+        self.slot_elems = int(np.prod(self.page_shape))
+        self.slot_bytes = self.slot_elems * self.slab.element_size()
+        self.valid_len = torch.zeros(capacity, dtype=torch.int32, device=self.device)
+        self._valid_host = np.zeros(capacity, dtype=np.int64)
+        self._by_id: dict[str, int] = {}
+        self._id_of: dict[int, str] = {}
+        self._free = list(range(capacity - 1, -1, -1))
+        self._lock = threading.Lock()
+
+    def grow(self, capacity: int) -> None:
+        """Re-home the slab with more slots (slot ids and handles stay valid)."""
+        import torch
+        with self._lock:
+            if capacity <= self.capacity:
+                return
+            slab = torch.empty((capacity, *self.page_shape), dtype=self.slab.dtype,
+                               device=self.device)
+            slab[:self.capacity].copy_(self.slab)
+            vl = torch.zeros(capacity, dtype=torch.int32, device=self.device)
+            vl[:self.capacity].copy_(self.valid_len)
+            hv = np.zeros(capacity, dtype=np.int64)
+            hv[:self.capacity] = self._valid_host
+            self._free = list(range(capacity - 1, self.capacity - 1, -1)) + self._free
+            self.slab, self.valid_len, self._valid_host = slab, vl, hv
+            self.capacity = capacity
+
+    # ---------------------------------------------------------- page table
+    def __len__(self) -> int:
+        return len(self._by_id)
+
+    def __contains__(self, chunk_id: str) -> bool:
+        return chunk_id in self._by_id
+
+    def allocate(self, chunk_ids) -> np.ndarray:
+        """Slots for new chunk ids (an existing id keeps its slot, like a put)."""
+        with self._lock:
+            out = np.empty(len(chunk_ids), dtype=np.int64)
+            for i, cid in enumerate(chunk_ids):
+                slot = self._by_id.get(cid)
+                if slot is None:
+                    if not self._free:
+                        raise StoreError(f"KV pool full ({self.capacity} slots)")
+                    slot = self._free.pop()
+                    self._by_id[cid] = slot
+                    self._id_of[slot] = cid
+                out[i] = slot
+            return out
+
+    def release(self, chunk_id: str) -> None:
+        with self._lock:
+            slot = self._by_id.pop(chunk_id, None)
+            if slot is not None:
+                self._id_of.pop(slot, None)
+                self._free.append(slot)
+
+    def lookup(self, chunk_ids) -> np.ndarray:
+        """chunk ids -> slots (-1 for a miss)."""
+        return np.array([self._by_id.get(c, -1) for c in chunk_ids], dtype=np.int64)
+
+    def chunk_ids(self) -> list[str]:
+        return sorted(self._by_id)
+
+    def slot_ptrs(self, slots):
+        """Device int64 tensor of slot base addresses for the kernels."""
+        import torch
+        s = torch.as_tensor(slots, device=self.device).to(torch.int64)
+        return s * self.slot_bytes + self.slab.data_ptr()
+
+    def set_valid_len(self, slots, valid_len) -> None:
+        import torch
+        slots = np.asarray(slots, dtype=np.int64)
+        vl = np.asarray(valid_len, dtype=np.int64)
+        self._valid_host[slots] = vl
+        self.valid_len[torch.as_tensor(slots, device=self.device)] = torch.as_tensor(
+            vl, dtype=torch.int32, device=self.device)
+
+    def host_valid_len(self, slot: int) -> int:
+        return int(self._valid_host[slot])
+
+    # ---------------------------------------------------------- host I/O
+    def write_host_kv(self, slot: int, keys: np.ndarray, values: np.ndarray,
+                      valid_len: int) -> None:
+        """Store f32 [L, KVH, D, HD] keys/values (e.g. a decoded HRKV entry)."""
+        import torch
+        L, _, KVH, D, HD = self.page_shape
+        if keys.shape != (L, KVH, D, HD) or values.shape != keys.shape:
+            raise ShapeError(f"cached KV shape {keys.shape} does not match pool "
+                             f"{(L, KVH, D, HD)}")
+        page = np.stack([np.asarray(keys, np.float32), np.asarray(values, np.float32)], axis=1)
+        self.slab[slot].copy_(torch.from_numpy(np.ascontiguousarray(page)).to(
+            self.device, non_blocking=False).to(self.slab.dtype))
+        self.set_valid_len([slot], [valid_len])
+
+    def read_host_kv(self, slot: int):
+        """(keys, values) as f32 numpy [L, KVH, D, HD]."""
+        page = self.slab[slot].float().cpu().numpy()
+        return np.ascontiguousarray(page[:, 0]), np.ascontiguousarray(page[:, 1])
+
+
+class HostKVTier:
+    """Pinned host-DRAM tier with the pool's slot layout, streamed into an HBM
+    staging pool on a side stream (cudaMemcpyAsync via torch copy_)."""
+
+    def __init__(self, pool_like: KVPool, capacity: int):
+        import torch
+        self.page_shape = pool_like.page_shape
+        self.dtype = pool_like.slab.dtype
+        self.capacity = capacity
+        self.slab = torch.empty((capacity, *self.page_shape), dtype=self.dtype, pin_memory=True)
+        self.slot_bytes = pool_like.slot_bytes
+        self.valid_len = np.zeros(capacity, dtype=np.int64)
+        self._by_id: dict[str, int] = {}
+        self._next = 0
+
+    def put_from_pool(self, chunk_id: str, pool: KVPool, slot: int) -> int:
+        if chunk_id not in self._by_id:
+            if self._next >= self.capacity:
+                raise StoreError("host tier full")
+            self._by_id[chunk_id] = self._next
+            self._next += 1
+        h = self._by_id[chunk_id]
+        self.slab[h].copy_(pool.slab[slot])
+        self.valid_len[h] = pool.host_valid_len(slot)
+        return h
+
+    def lookup(self, chunk_ids) -> np.ndarray:
+        return np.array([self._by_id.get(c, -1) for c in chunk_ids], dtype=np.int64)
+
+    def stream_in(self, host_slots, staging: KVPool, staging_slots, stream) -> None:
+        """Queue H2D copies of host pages into staging pool slots on ``stream``."""
+        import torch
+        with torch.cuda.stream(stream):
+            for h, s in zip(host_slots, staging_slots):
+                staging.slab[int(s)].copy_(self.slab[int(h)], non_blocking=True)
+        staging.set_valid_len(staging_slots, self.valid_len[np.asarray(host_slots)])

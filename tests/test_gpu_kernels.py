@@ -1,0 +1,221 @@
+"""Kernel-level numerics on the device, each against a plain PyTorch fp32
+reference of the same op (and the oracle for the weight streams)."""
+
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2504_02921_b200 import _lib  # noqa: E402
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.manual_seed(0)
+
+
+def test_library_loads_on_device():
+    assert _lib.lib().krr_version().startswith(b"kvrerank_b200")
+
+
+@pytest.mark.parametrize("code,tdt", [(_lib.F32, torch.float32), (_lib.F16, torch.float16)])
+def test_init_uniform_matches_oracle(code, tdt):
+    import oracle
+    rows, cols = 96, 160
+    seed = 0 ^ oracle.fnv1a64("layers.0.attn.wq")
+    bound = math.sqrt(6.0 / (rows + cols))
+    ref = oracle.uniform_signed(seed, rows * cols, bound).reshape(rows, cols)
+    out = torch.empty((cols, rows), dtype=tdt, device="cuda")   # transposed [out, in]
+    _lib.check(_lib.lib().krr_init_uniform(seed, bound, rows, cols, 1, code, out.data_ptr(),
+                                           rows, _stream()))
+    got = out.float().cpu().numpy().T
+    want = ref.astype(np.float16).astype(np.float32) if code == _lib.F16 else ref
+    assert np.array_equal(got, want)
+
+
+def _gemm(backend, act, A, B, epi, out, qkv=None):
+    _lib.check(_lib.lib().krr_gemm(backend, act, A.data_ptr(), B.data_ptr(), A.shape[0],
+                                   B.shape[0], A.shape[1], epi,
+                                   out.data_ptr() if out is not None else 0,
+                                   C.byref(qkv) if qkv is not None else None, _stream()))
+
+
+GEMM_SHAPES = [(128, 256, 64), (300, 512, 256), (1000, 1024, 512), (77, 96, 128),
+               (2048, 4096, 1024)]
+
+
+@pytest.mark.parametrize("backend", [_lib.GEMM_TCGEN05, _lib.GEMM_SIMT])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_store_gelu_residual(backend, M, N, K):
+    A = (torch.randn(M, K, device="cuda") * 0.5).half()
+    B = (torch.randn(N, K, device="cuda") * (1.0 / math.sqrt(K))).half()
+    ref = A.float() @ B.float().T
+    out = torch.empty(M, N, dtype=torch.float16, device="cuda")
+    _gemm(backend, _lib.F16, A, B, _lib.EPI_STORE, out)
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-3 * max(1.0, ref.abs().max().item()), err
+    _gemm(backend, _lib.F16, A, B, _lib.EPI_GELU, out)
+    g = torch.nn.functional.gelu(ref, approximate="tanh")
+    torch.cuda.synchronize()
+    assert (out.float() - g).abs().max().item() <= 2e-3 * max(1.0, g.abs().max().item())
+    x = torch.randn(M, N, device="cuda")
+    x0 = x.clone()
+    _gemm(backend, _lib.F16, A, B, _lib.EPI_RESIDUAL, x)
+    torch.cuda.synchronize()
+    assert (x - (x0 + ref)).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
+
+
+def test_gemm_f32_simt_exact_order():
+    M, N, K = 200, 128, 96
+    A = torch.randn(M, K, device="cuda")
+    B = torch.randn(N, K, device="cuda")
+    out = torch.empty(M, N, device="cuda")
+    _gemm(_lib.GEMM_SIMT, _lib.F32, A, B, _lib.EPI_STORE, out)
+    ref = (A.double() @ B.double().T).float()
+    torch.cuda.synchronize()
+    assert (out - ref).abs().max().item() < 1e-4
+
+
+def test_gemm_batch_invariance_tcgen05():
+    """A row's result must not depend on M (no split-K): SPEC.md:178."""
+    K, N = 512, 768
+    A = (torch.randn(1000, K, device="cuda") * 0.5).half()
+    B = (torch.randn(N, K, device="cuda") * 0.05).half()
+    full = torch.empty(1000, N, dtype=torch.float16, device="cuda")
+    _gemm(_lib.GEMM_TCGEN05, _lib.F16, A, B, _lib.EPI_STORE, full)
+    part = torch.empty(333, N, dtype=torch.float16, device="cuda")
+    _gemm(_lib.GEMM_TCGEN05, _lib.F16, A[500:833].contiguous(), B, _lib.EPI_STORE, part)
+    torch.cuda.synchronize()
+    assert torch.equal(full[500:833], part)
+
+
+def _rope_ref(x, pos, cos, sin):
+    # x [..., HD] rotated as complex pairs (model.py:144,370-371)
+    a, b = x[..., 0::2], x[..., 1::2]
+    c, s = cos[pos], sin[pos]
+    out = torch.empty_like(x)
+    out[..., 0::2] = a * c - b * s
+    out[..., 1::2] = a * s + b * c
+    return out
+
+
+@pytest.mark.parametrize("backend", [_lib.GEMM_TCGEN05, _lib.GEMM_SIMT])
+def test_gemm_qkv_rope_scatter(backend):
+    from paper_2504_02921_b200.model import rope_tables
+    H, KVH, HD, T, nseq, L, layer = 4, 2, 64, 48, 3, 2, 1
+    d = H * HD
+    G = H // KVH
+    M = nseq * T
+    N = (H + 2 * KVH) * HD
+    pos0 = 128
+    cos, sin = rope_tables(10000.0, HD, 1024)
+    cos_t, sin_t = torch.from_numpy(cos).cuda(), torch.from_numpy(sin).cuda()
+    A = (torch.randn(M, d, device="cuda")).half()
+    B = (torch.randn(N, d, device="cuda") / 16).half()
+    ref = A.float() @ B.float().T
+    q_out = torch.zeros(nseq * KVH * G * T * HD, dtype=torch.float16, device="cuda")
+    slabs = torch.zeros(nseq, L, 2, KVH, T, HD, dtype=torch.float16, device="cuda")
+    ptrs = torch.arange(nseq, device="cuda", dtype=torch.int64) * (slabs[0].numel() * 2) + \
+        slabs.data_ptr()
+    qkv = _lib.QKV(H, KVH, HD, T, pos0, layer, T, cos_t.data_ptr(), sin_t.data_ptr(),
+                   q_out.data_ptr(), ptrs.data_ptr())
+    _gemm(backend, _lib.F16, A, B, _lib.EPI_QKV_ROPE, None, qkv)
+    torch.cuda.synchronize()
+    pos = torch.arange(T, device="cuda") + pos0
+    r = ref.view(nseq, T, H + 2 * KVH, HD)
+    q = _rope_ref(r[:, :, :H], pos[None, :, None].expand(nseq, T, H), cos_t, sin_t)
+    k = _rope_ref(r[:, :, H:H + KVH], pos[None, :, None].expand(nseq, T, KVH), cos_t, sin_t)
+    v = r[:, :, H + KVH:]
+    q_want = q.view(nseq, T, KVH, G, HD).permute(0, 2, 3, 1, 4).reshape(-1)
+    assert (q_out.float() - q_want).abs().max().item() < 2e-2
+    assert (slabs[:, layer, 0].float() - k.permute(0, 2, 1, 3)).abs().max().item() < 2e-2
+    assert (slabs[:, layer, 1].float() - v.permute(0, 2, 1, 3)).abs().max().item() < 2e-2
+    assert slabs[:, 1 - layer].abs().max().item() == 0
+
+
+def _attn_ref(q, kp, vp, vlen, kc, vc, tv, G, T):
+    """fp32 torch restatement of model.py:373-394 for one (seq, kv head)."""
+    P = kp.shape[0]
+    logits_p = q @ kp.T
+    logits_c = q @ kc.T
+    t = torch.arange(G * T, device=q.device) % T
+    pm = torch.arange(P, device=q.device)[None, :] < vlen
+    cm = (torch.arange(T, device=q.device)[None, :] <= t[:, None]) & tv[None, :].bool()
+    logits_p = logits_p.masked_fill(~pm, float("-inf"))
+    logits_c = logits_c.masked_fill(~cm, float("-inf"))
+    lg = torch.cat([logits_p, logits_c], dim=1)
+    m = lg.max(dim=1, keepdim=True).values
+    m = torch.where(torch.isfinite(m), m, torch.zeros_like(m))
+    e = torch.exp(lg - m)
+    z = e.sum(dim=1, keepdim=True)
+    z = torch.where(z == 0, torch.ones_like(z), z)
+    return (e @ torch.cat([vp, vc], dim=0)) / z
+
+
+@pytest.mark.parametrize("HD,G,KVH,P,T", [(64, 2, 2, 128, 48), (128, 4, 2, 512, 48),
+                                          (256, 8, 1, 512, 48), (64, 2, 2, 0, 128),
+                                          (128, 4, 2, 0, 100)])
+@pytest.mark.parametrize("backend,act", [(_lib.ATTN_TC, _lib.F16), (_lib.ATTN_SIMT, _lib.F32),
+                                         (_lib.ATTN_TC, _lib.BF16)])
+def test_attention(HD, G, KVH, P, T, backend, act):
+    nseq, L, layer = 3, 2, 1
+    tdt = {_lib.F16: torch.float16, _lib.F32: torch.float32, _lib.BF16: torch.bfloat16}[act]
+    sc = 1.0 / math.sqrt(math.sqrt(HD))
+    q = (torch.randn(nseq * KVH, G * T, HD, device="cuda") * sc).to(tdt)
+    pre = (torch.randn(nseq, L, 2, KVH, max(P, 1), HD, device="cuda") * sc).to(tdt)
+    cur = (torch.randn(nseq, 1, 2, KVH, T, HD, device="cuda") * sc).to(tdt)
+    vlen = torch.tensor([P, max(1, P // 3), max(1, P - 7)][:nseq], dtype=torch.int32,
+                        device="cuda")
+    tv = torch.ones(nseq, T, dtype=torch.uint8, device="cuda")
+    tv[1, T - 5:] = 0
+    tv[2, 3] = 0
+    tv[2, 10] = 0
+    es = pre.element_size()
+    pptr = torch.arange(nseq, device="cuda", dtype=torch.int64) * (pre[0].numel() * es) + \
+        pre.data_ptr()
+    cptr = torch.arange(nseq, device="cuda", dtype=torch.int64) * (cur[0].numel() * es) + \
+        cur.data_ptr()
+    H = KVH * G
+    out = torch.zeros(nseq * T, H * HD, dtype=tdt, device="cuda")
+    _lib.check(_lib.lib().krr_attention(backend, act, q.data_ptr(), nseq, KVH, G, HD, T, P,
+                                        layer, 0, pptr.data_ptr(), vlen.data_ptr(),
+                                        cptr.data_ptr(), tv.data_ptr(), out.data_ptr(),
+                                        _stream()))
+    torch.cuda.synchronize()
+    tol = {_lib.F16: 2e-2, _lib.BF16: 6e-2, _lib.F32: 1e-4}[act]
+    for b in range(nseq):
+        for kh in range(KVH):
+            kp = pre[b, layer, 0, kh, :P].float()
+            vp = pre[b, layer, 1, kh, :P].float()
+            ref = _attn_ref(q[b * KVH + kh].float(), kp, vp, int(vlen[b]) if P else 0,
+                            cur[b, 0, 0, kh].float(), cur[b, 0, 1, kh].float(), tv[b], G, T)
+            got = out.view(nseq, T, KVH, G, HD)[b, :, kh].permute(1, 0, 2).reshape(G * T, HD)
+            err = (got.float() - ref).abs().max().item()
+            assert err <= tol * max(1.0, ref.abs().max().item()), (b, kh, err)
+
+
+def test_segmented_topk():
+    n_seg, seg, k = 5, 100, 20
+    s = torch.randn(n_seg, seg, device="cuda")
+    s[0, 10] = s[0, 20] = s[0, 30] = 5.0   # ties broken by doc id
+    ids = torch.stack([torch.randperm(1000, device="cuda")[:seg] for _ in range(n_seg)]).int()
+    idx = torch.empty(n_seg, k, dtype=torch.int32, device="cuda")
+    sc = torch.empty(n_seg, k, device="cuda")
+    _lib.check(_lib.lib().krr_segmented_topk(s.data_ptr(), ids.data_ptr(), n_seg, seg, k,
+                                             idx.data_ptr(), sc.data_ptr(), _stream()))
+    torch.cuda.synchronize()
+    s_h, ids_h = s.cpu().numpy(), ids.cpu().numpy()
+    for i in range(n_seg):
+        want = sorted(range(seg), key=lambda j: (-s_h[i, j], ids_h[i, j]))[:k]
+        assert idx[i].cpu().tolist() == want

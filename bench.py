@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""Benchmark: reranked query-doc pairs/s (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+    python bench.py --impl reference ...      # the reference CPU path (oracle port)
+
+One step = one rerank batch of the configured workload: every (query,
+candidate) pair's query suffix is run on top of the candidate's cached
+document KV (HBM pool), scores go through the per-query top-k, and with N>1
+GPUs each rank scores its own document shard and a NCCL all-gather merges the
+per-rank top-k.  Default workload (N=1): BASELINE configs[2], the
+Mistral-7B-shape reranker, 64 queries x 100 docs x 512 tokens, Q=48.
+
+Prints ONE JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reranked query-doc pairs/sec"
+CONFIGS = {
+    # name: (preset, corpus docs per GPU, queries, candidates per query per GPU, keep)
+    "c1": ("c1_tiny", 64, 1, 64, 20),
+    "c2": ("c2_gemma2b", 100, 1, 100, 20),
+    "c3": ("c3_mistral7b", 1000, 64, 100, 20),
+}
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x20: "sync_boost", 0x40: "sw_thermal_slowdown",
+           0x80: "hw_thermal_slowdown", 0x100: "hw_power_brake_slowdown",
+           0x200: "display_clock_setting"}
+
+
+def suffix_flops_per_pair(cfg, D, Q):
+    """2*L*P_layer*Q + 4*L*H*HD*sum_{j=1..Q}(D+j)."""
+    d, H, KVH, HD, L = cfg.model_dim, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.layers
+    p_layer = d * (H + 2 * KVH) * HD + H * HD * d + 8 * d * d
+    return 2 * L * p_layer * Q + 4 * L * H * HD * sum(D + j for j in range(1, Q + 1))
+
+
+def kv_bytes_per_pair(cfg, D, es=2):
+    return 2 * cfg.layers * cfg.kv_heads * D * cfg.head_dim * es
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), \
+            p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        try:
+            with open(self.f.name) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) < 4:
+                        continue
+                    try:
+                        s, m = float(parts[0]), float(parts[1])
+                        bits = int(parts[3], 16)
+                    except ValueError:
+                        continue
+                    sm.append(s)
+                    mx = max(mx, m)
+                    for bit, name in REASONS.items():
+                        if bits & bit and name != "gpu_idle":
+                            reasons.add(name)
+            os.unlink(self.f.name)
+        except OSError:
+            pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_pairs_per_s(preset, D, Q, budget_s=12.0, max_pairs=8):
+    """Time the oracle port (numpy restatement of the reference forward) on this
+    host.  Small models: whole forward per pair.  7B/Gemma shapes: one layer
+    per pair (weights of that one layer from the reference init), scaled by L."""
+    import oracle
+    from paper_2504_02921_b200.config import PRESETS
+    cfg, lay = PRESETS[preset]
+    ocfg = oracle.OracleConfig(layers=cfg.layers, model_dim=cfg.model_dim, heads=cfg.heads,
+                               kv_heads=cfg.kv_heads, head_dim=cfg.head_dim,
+                               vocab_size=cfg.vocab_size, max_position=cfg.max_position,
+                               document_len=D, query_len=Q)
+    rng = np.random.default_rng(3)
+    per_layer = cfg.model_dim >= 1024
+    if per_layer:
+        one = oracle.OracleConfig(**{**ocfg.__dict__, "layers": 1})
+        w = oracle.init_weights(one, with_embedding=False)
+        kvh, hd = cfg.kv_heads, cfg.head_dim
+        past_k = rng.standard_normal((1, kvh, D, hd)).astype(np.float32)
+        past_v = rng.standard_normal((1, kvh, D, hd)).astype(np.float32)
+        x0 = rng.standard_normal((Q, cfg.model_dim)).astype(np.float32)
+        toks = rng.integers(1, cfg.vocab_size, Q)
+        pos = np.arange(D, D + Q)
+        oracle.forward(w, toks, pos, past_k, past_v, None, x_in=x0)  # warm
+        t0, n = time.perf_counter(), 0
+        while n < max_pairs and (time.perf_counter() - t0) < budget_s:
+            oracle.forward(w, toks, pos, past_k, past_v, None, x_in=x0)
+            n += 1
+        t = (time.perf_counter() - t0) / n * cfg.layers
+        sample = f"{n} pairs x 1 of {cfg.layers} layers (D={D}, Q={Q}), time x{cfg.layers}"
+    else:
+        w = oracle.init_weights(ocfg)
+        docs = rng.integers(1, cfg.vocab_size, (max_pairs, D))
+        q = rng.integers(1, cfg.vocab_size, Q)
+        kvs = [oracle.doc_prefill(w, d) for d in docs[:2]]
+        oracle.score_reuse(w, *kvs[0], q)
+        t0, n = time.perf_counter(), 0
+        while n < 64 and (time.perf_counter() - t0) < budget_s:
+            oracle.score_reuse(w, *kvs[n % 2], q)
+            n += 1
+        t = (time.perf_counter() - t0) / n
+        sample = f"{n} reuse pairs, full {cfg.layers}-layer forward (D={D}, Q={Q})"
+    cores = len(os.sched_getaffinity(0))
+    return 1.0 / t, {"cores": cores, "kind": "port", "sample": sample,
+                     "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS", f"default ({cores})")}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port), rank 0 only."""
+    if rank != 0:
+        return
+    preset, corpus, nq, nc, keep = CONFIGS[args.config]
+    from paper_2504_02921_b200.config import PRESETS
+    cfg, lay = PRESETS[preset]
+    D, Q = lay.document_len, lay.query_len
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_pairs_per_s(preset, D, Q, budget_s=4.0, max_pairs=2)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * nq * nc * args.gpus / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, cfg, lay, corpus, nq, nc, keep),
+        "cpu_baseline": {"value": value, "unit": "pairs/s", **info},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def workload_config(args, cfg, lay, corpus, nq, nc, keep):
+    return {"workload": f"{CONFIGS[args.config][0]}: {nq} queries x {nc * args.gpus} docs x "
+                        f"{lay.document_len} tok, query suffix {lay.query_len}, "
+                        f"corpus {corpus} docs/GPU HBM-resident",
+            "layers": cfg.layers, "model_dim": cfg.model_dim, "heads": cfg.heads,
+            "kv_heads": cfg.kv_heads, "head_dim": cfg.head_dim, "mlp": "gelu_tanh 4d",
+            "queries": nq, "candidates_per_query": nc * args.gpus, "doc_len": lay.document_len,
+            "query_len": lay.query_len, "corpus_docs_per_gpu": corpus, "keep": keep,
+            "parallelism": f"doc-shard x{args.gpus} + NCCL all-gather top-k"
+            if args.gpus > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (KV pool + weights >> 126 MB), no flush"}
+
+
+# ----------------------------------------------------------------- GPU leg
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2504_02921_b200 as krr
+    from paper_2504_02921_b200 import _lib, engine, pipeline
+    from paper_2504_02921_b200.config import PRESETS
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    preset, corpus, nq, nc, keep = CONFIGS[args.config]
+    corpus = args.corpus or corpus
+    nq = args.queries or nq
+    nc = args.cands or nc
+    cfg, lay = PRESETS[preset]
+    D, Q = lay.document_len, lay.query_len
+    t_build = time.perf_counter()
+    model = krr.RerankModel.build(cfg, lay, precision=args.precision, device=dev)
+    w = model.weights
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+
+    # ---- corpus shard: docs with global id rank*corpus + i, prefilled into the HBM pool
+    pool = krr.KVPool(cfg, D, corpus, w.dtype, dev)
+    rng = np.random.default_rng(1000 + rank)
+    docs = rng.integers(1, cfg.vocab_size, (corpus, D), dtype=np.int64)
+    ids = [f"doc-{rank * corpus + i:06d}" for i in range(corpus)]
+    slots = pool.allocate(ids)
+    engine.prefill_slots(w, pool, slots, docs, np.full(corpus, D))  # warm-up / compile
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    engine.prefill_slots(w, pool, slots, docs, np.full(corpus, D))
+    torch.cuda.synchronize()
+    prefill_s = time.perf_counter() - t0
+
+    # ---- queries (broadcast: same on every rank) and per-rank candidates
+    qrng = np.random.default_rng(7)
+    q_host = qrng.integers(1, cfg.vocab_size, (nq, Q), dtype=np.int64)
+    crng = np.random.default_rng(100 + rank)
+    cand_local = np.stack([crng.choice(corpus, nc, replace=False) for _ in range(nq)])
+    cand_ids = [[ids[j] for j in row] for row in cand_local]
+    q_dev = torch.as_tensor(q_host.astype(np.int32), device=dev)
+    slots_dev = torch.as_tensor(slots[cand_local.reshape(-1)], device=dev)
+    qidx = torch.arange(nq, device=dev).repeat_interleave(nc)
+    gid_dev = torch.as_tensor((rank * corpus + cand_local).reshape(-1).astype(np.int32),
+                              device=dev)
+    k = min(keep, nc)
+    scores = torch.empty(nq * nc, dtype=torch.float32, device=dev)
+
+    def merge(idx, sc):
+        """Global top-k: all-gather per-rank (score, doc id), merge on device."""
+        gid = gid_dev.view(nq, nc).gather(1, idx.long())
+        if world == 1:
+            return gid, sc
+        all_sc = [torch.empty_like(sc) for _ in range(world)]
+        all_id = [torch.empty_like(gid) for _ in range(world)]
+        dist.all_gather(all_sc, sc.contiguous())
+        dist.all_gather(all_id, gid.contiguous())
+        cs, ci = torch.cat(all_sc, 1).contiguous(), torch.cat(all_id, 1).contiguous()
+        midx, msc = engine.segmented_topk(cs.view(-1), ci.view(-1), nq, world * k, k)
+        return ci.gather(1, midx.long()), msc
+
+    def step():
+        engine.score_slots(w, pool, slots_dev, q_dev.index_select(0, qidx), out=scores)
+        idx, sc = engine.segmented_topk(scores, gid_dev, nq, nc, k)
+        return merge(idx, sc)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = _lib.launch_count()
+    _lib.profile_enable(True)
+    with Clocks(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    launches = _lib.launch_count() - n_launch0
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    pairs_step = nq * nc * world
+    value = pairs_step * args.steps / (ms / 1e3)
+
+    # ---- e2e through the public API (host inputs -> host top-k), max over ranks
+    def e2e_step():
+        res = pipeline.rerank(model, pool, [f"q{i}" for i in range(nq)], q_host, cand_ids, k)
+        if world > 1:
+            sc = torch.tensor([[p.score for p in r] for r in res.selected], device=dev)
+            gi = torch.tensor([[int(p.chunk_id[4:]) for p in r] for r in res.selected],
+                              dtype=torch.int32, device=dev)
+            all_sc = [torch.empty_like(sc) for _ in range(world)]
+            all_id = [torch.empty_like(gi) for _ in range(world)]
+            dist.all_gather(all_sc, sc)
+            dist.all_gather(all_id, gi)
+            cs, ci = torch.cat(all_sc, 1).contiguous(), torch.cat(all_id, 1).contiguous()
+            midx, msc = engine.segmented_topk(cs.view(-1), ci.view(-1), nq, world * k, k)
+            ci.gather(1, midx.long()).cpu()
+        return res
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    barrier()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = pairs_step * args.steps / (float(t.item()) / 1e3)
+    # bytes the public call moves per step (counted from the tensors it copies)
+    h2d = nq * Q * 4 + nq * nc * (8 + 8 + 4)      # query tokens, slots, pair->query idx, doc ranks
+    d2h = nq * k * (4 + 4)                         # top-k indices + scores
+
+    out = None
+    if rank == 0:
+        # ---- p50 per-query latency (1 query x all candidates, public API)
+        lat = []
+        for i in range(args.latency_reps + 2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pipeline.rerank(model, pool, ["q"], q_host[:1], cand_ids[:1], k)
+            torch.cuda.synchronize()
+            if i >= 2:
+                lat.append((time.perf_counter() - t0) * 1e3)
+        # ---- same-box full-recompute GPU baseline (prefill + suffix, same kernels)
+        nf = min(args.full_pairs, corpus)
+        st = krr.KVPool(cfg, D, nf, w.dtype, dev)
+        st_slots = st.allocate([f"f{i}" for i in range(nf)])
+
+        def full_step():
+            engine.prefill_slots(w, st, st_slots, docs[:nf], np.full(nf, D))
+            engine.score_slots(w, st, st_slots, q_dev[:1].expand(nf, Q))
+        full_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(2):
+            full_step()
+        torch.cuda.synchronize()
+        full_pps = 2 * nf / (time.perf_counter() - t0)
+        del st
+
+        peak_b, peak_s, hbm, peak_kind = load_peaks()
+        gemm_tf = prof["gemm_flops"] / (prof["gemm_ms"] / 1e3) / 1e12 if prof["gemm_ms"] else 0
+        f_pair = suffix_flops_per_pair(cfg, D, Q)
+        roof_pps = min(peak_s * 1e12 / f_pair, hbm * 1e9 / kv_bytes_per_pair(cfg, D))
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        cpu = None
+        if not args.no_cpu_baseline:
+            v, info = cpu_pairs_per_s(preset, D, Q)
+            cpu = {"value": v, "unit": "pairs/s", **info}
+        step_ms = ms / args.steps
+        out = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic (reference random-init weights, seed 0; "
+                                              "uniform token ids)",
+            "config": workload_config(args, cfg, lay, corpus, nq, nc, keep),
+            "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "paper_2504_02921_b200.pipeline.rerank"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "roofline": {"bound": "tensor", "kernel": "gemm_tcgen05 (QKV/WO/MLP-up/MLP-down)",
+                         "achieved": gemm_tf, "peak": peak_s, "unit": "TFLOP/s",
+                         "frac": gemm_tf / peak_s if peak_s else None, "traffic": traffic,
+                         "peak_kind": f"{peak_kind} bf16 sustained (dense f16 same rate)",
+                         "gemm_share_of_step": prof["gemm_ms"] / ms if ms else None,
+                         "attn_share_of_step": prof["attn_ms"] / ms if ms else None,
+                         "misc_share_of_step": prof["misc_ms"] / ms if ms else None,
+                         "pairs_roofline": roof_pps, "pairs_frac": value / world / roof_pps},
+            "cpu_baseline": cpu,
+            "p50_query_latency_ms": float(np.median(lat)) if lat else None,
+            "p50_query_latency_candidates": nc,
+            "full_recompute_pairs_per_s": full_pps,
+            "reuse_over_full": value / world / full_pps,
+            "prefill_docs_per_s": corpus / prefill_s,
+            "model_build_s": t_build,
+        }
+        print(json.dumps(out))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="f16", choices=["f16", "bf16"])
+    ap.add_argument("--corpus", type=int, default=0)
+    ap.add_argument("--queries", type=int, default=0)
+    ap.add_argument("--cands", type=int, default=0)
+    ap.add_argument("--latency-reps", type=int, default=20)
+    ap.add_argument("--full-pairs", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

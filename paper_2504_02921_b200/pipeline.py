@@ -1,0 +1,100 @@
+"""Rerank + select stage of the reference pipeline on the device.
+
+Restates the scoring and selection stages of handle_query
+(pipeline.py:274-287, 297-326) for many queries at once:
+
+  candidates (chunk ids) --page-table lookup--> pool slots      (_fetch_items, :251-271)
+  every (query, candidate) pair scored in one batch             (_score_item, :274-282)
+  per-query top-keep_m by (-score, chunk_id) on the device      (_select, :285-287)
+
+A candidate whose KV is not resident (cache miss) falls back to full
+recompute for that pair, exactly like the reference (:258-265); misses are
+counted.  Doc ids passed to the top-k kernel are ranks in sorted chunk-id
+order, so the integer tie-break equals the reference's string tie-break.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import engine
+from .errors import ConfigError, ShapeError
+from .kvpool import KVPool
+from .model import RerankModel
+from .reranker import ScoredPair, _doc_valid
+
+
+@dataclass
+class RerankResult:
+    query_ids: list
+    selected: list          # per query: list[ScoredPair] (best first)
+    cache_misses: int
+    pairs: int
+
+
+def _id_ranks(chunk_ids_2d) -> np.ndarray:
+    flat = sorted(set(c for row in chunk_ids_2d for c in row))
+    rank = {c: i for i, c in enumerate(flat)}
+    return np.array([[rank[c] for c in row] for row in chunk_ids_2d], dtype=np.int32)
+
+
+def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates, keep_m: int,
+           doc_tokens: dict | None = None, path: str = "fast") -> RerankResult:
+    """Score every candidate of every query against its cached document KV
+    and keep the best ``keep_m`` per query.
+
+    query_tokens: int [n_q, Q] host array; candidates: n_q lists of equal
+    length of chunk ids; doc_tokens: chunk_id -> tokens for miss fallback."""
+    import torch
+    if keep_m < 1:
+        raise ConfigError("keep_m must be >= 1")
+    w = model.weights_for(path)
+    q = np.asarray(query_tokens)
+    n_q = len(query_ids)
+    if q.shape != (n_q, model.layout.query_len):
+        raise ShapeError(f"query tokens must be [{n_q}, {model.layout.query_len}]")
+    if any((row != 0).sum() == 0 for row in q):
+        from .errors import DegenerateInputError
+        raise DegenerateInputError("query is entirely padding")
+    n_c = len(candidates[0]) if n_q else 0
+    if any(len(c) != n_c for c in candidates):
+        raise ShapeError("every query needs the same number of candidates")
+    flat = [c for row in candidates for c in row]
+    slots = pool.lookup(flat)
+    miss = np.nonzero(slots < 0)[0]
+    dev = w.device
+    scores = torch.empty(n_q * n_c, dtype=torch.float32, device=dev)
+    hit = np.nonzero(slots >= 0)[0]
+    q_dev = torch.as_tensor(q.astype(np.int32), device=dev)
+    if len(hit):
+        qi = torch.as_tensor(hit // n_c, device=dev)
+        sc = engine.score_slots(w, pool, torch.as_tensor(slots[hit], device=dev),
+                                q_dev.index_select(0, qi))
+        scores[torch.as_tensor(hit, device=dev)] = sc
+    if len(miss):
+        if doc_tokens is None:
+            raise ShapeError("cache miss without doc_tokens for full-recompute fallback")
+        docs = np.stack([np.asarray(doc_tokens[flat[i]]) for i in miss])
+        for dd in docs:
+            _doc_valid(model, dd)
+        stage = KVPool(model.config, model.layout.document_len, len(miss), w.dtype, dev)
+        st_slots = stage.allocate([f"__miss_{i}" for i in range(len(miss))])
+        engine.prefill_slots(w, stage, st_slots, docs, (docs != 0).sum(axis=1))
+        qi = torch.as_tensor(miss // n_c, device=dev)
+        scores[torch.as_tensor(miss, device=dev)] = engine.score_slots(
+            w, stage, st_slots, q_dev.index_select(0, qi))
+    ids = _id_ranks(candidates)
+    k = min(keep_m, n_c)
+    idx, sc = engine.segmented_topk(scores, ids.reshape(-1), n_q, n_c, k)
+    idx_h, sc_h = idx.cpu().numpy(), sc.cpu().numpy()
+    selected = [[ScoredPair(chunk_id=candidates[i][int(j)], query_id=query_ids[i],
+                            score=float(s)) for j, s in zip(idx_h[i], sc_h[i]) if j >= 0]
+                for i in range(n_q)]
+    return RerankResult(list(query_ids), selected, int(len(miss)), n_q * n_c)
+
+
+def select(scored: list[ScoredPair], keep_m: int) -> list[ScoredPair]:
+    """Host form of _select (pipeline.py:285-287)."""
+    return sorted(scored, key=lambda p: (-p.score, p.chunk_id))[:keep_m]

@@ -283,10 +283,12 @@ def run_ours(args, rank, world, local_rank):
     n_launch0 = _lib.launch_count()
     _lib.profile_enable(True)
     with Clocks(local_rank) as clk:
+        torch.cuda.nvtx.range_push("timed")
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
+        torch.cuda.nvtx.range_pop()
         barrier()
     launches = _lib.launch_count() - n_launch0
     prof = _lib.profile_read()

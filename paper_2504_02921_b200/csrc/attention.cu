@@ -29,7 +29,7 @@ namespace attn_simt {
 constexpr int WARPS = 4;
 
 template <typename T>
-__global__ void __launch_bounds__(WARPS * 32) kernel(AttnParams p) {
+__global__ void __launch_bounds__(WARPS * 32) attn_prefix_simt(AttnParams p) {
   extern __shared__ float sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.group, T_ = p.seq_len, P = p.prefix_len, HD = p.head_dim;
@@ -97,14 +97,14 @@ int launch_attention_simt(int act_dtype, const AttnParams& p, cudaStream_t s) {
   const size_t smem = (size_t)WARPS * (p.prefix_len + p.seq_len + p.head_dim) * sizeof(float);
   KRR_REQUIRE(smem <= 200 * 1024, KRR_ESHAPE, "SIMT attention: sequence too long");
   if (act_dtype == KRR_F32) {
-    cudaFuncSetAttribute(kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kernel<float><<<grid, WARPS * 32, smem, s>>>(p);
+    cudaFuncSetAttribute(attn_prefix_simt<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attn_prefix_simt<float><<<grid, WARPS * 32, smem, s>>>(p);
   } else if (act_dtype == KRR_F16) {
-    cudaFuncSetAttribute(kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kernel<__half><<<grid, WARPS * 32, smem, s>>>(p);
+    cudaFuncSetAttribute(attn_prefix_simt<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attn_prefix_simt<__half><<<grid, WARPS * 32, smem, s>>>(p);
   } else {
-    cudaFuncSetAttribute(kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kernel<__nv_bfloat16><<<grid, WARPS * 32, smem, s>>>(p);
+    cudaFuncSetAttribute(attn_prefix_simt<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attn_prefix_simt<__nv_bfloat16><<<grid, WARPS * 32, smem, s>>>(p);
   }
   return check_launch("attention_simt");
 }
@@ -112,8 +112,8 @@ int launch_attention_simt(int act_dtype, const AttnParams& p, cudaStream_t s) {
 // ============================================================ mma.sync (16-bit)
 namespace attn_mma {
 
-constexpr int ROWS = 64;     // query rows per CTA (4 warps x 16)
-constexpr int THREADS = 128;
+
+
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -164,42 +164,48 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   }
 }
 
-// HD = head dim, KB = keys per block.  Row pitch HD+8 elements (16B pad) keeps
+
+// One CTA per (sequence, kv head) unit — or per slice of its G*T rows when
+// that exceeds max_warps*16 — so every K/V block is fetched into shared
+// memory once and reused by all query rows of the unit (all G heads of the
+// GQA group).  Warp w owns 16 rows.  K/V blocks of KB keys stream through a
+// STAGES-deep cp.async ring; row pitch HD+8 elements (16 B pad) keeps
 // ldmatrix conflict-free.
+constexpr int STAGES = 3;
+
 template <typename T, int HD, int KB>
-__global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) {
+__global__ void __launch_bounds__(384, 1) attn_prefix_mma(AttnParams p, int row_blocks) {
   constexpr int PITCH = HD + 8;
+  constexpr int CPR = HD / 8;  // 16 B chunks per row
   extern __shared__ __align__(16) uint8_t smem[];
+  const int nwarps = blockDim.x >> 5;
+  const int rows_cta = nwarps * 16;
   T* sQ = reinterpret_cast<T*>(smem);
-  T* sK = sQ + ROWS * PITCH;             // [2][KB][PITCH]
-  T* sV = sK + 2 * KB * PITCH;           // [2][KB][PITCH]
-  uint8_t* sTV = reinterpret_cast<uint8_t*>(sV + 2 * KB * PITCH);  // [T]
+  T* sK = sQ + rows_cta * PITCH;                 // [STAGES][KB][PITCH]
+  T* sV = sK + STAGES * KB * PITCH;              // [STAGES][KB][PITCH]
+  uint8_t* sTV = reinterpret_cast<uint8_t*>(sV + STAGES * KB * PITCH);  // [T]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nthr = blockDim.x;
   const int G = p.group, T_ = p.seq_len, P = p.prefix_len, KVH = p.kv_heads;
   const int unit = blockIdx.x / row_blocks;
   const int rb = blockIdx.x - unit * row_blocks;
   const int b = unit / KVH, kvh = unit - b * KVH;
-  const int row0 = rb * ROWS;
+  const int row0 = rb * rows_cta;
   const int nrows = G * T_;
 
-  // ---- Q tile + current-token validity into smem
   const T* qg = reinterpret_cast<const T*>(p.q) + ((int64_t)unit * nrows) * HD;
-  constexpr int CPR = HD / 8;  // 16B chunks per row
-  for (int i = threadIdx.x; i < ROWS * CPR; i += THREADS) {
+  for (int i = threadIdx.x; i < rows_cta * CPR; i += nthr) {
     const int r = i / CPR, c = (i - r * CPR) * 8;
     const bool ok = row0 + r < nrows;
     cp_async16(sQ + r * PITCH + c, qg + (int64_t)(ok ? row0 + r : 0) * HD + c, ok);
   }
-  for (int j = threadIdx.x; j < T_; j += THREADS) sTV[j] = p.tok_valid[(int64_t)b * T_ + j];
+  for (int j = threadIdx.x; j < T_; j += nthr) sTV[j] = p.tok_valid[(int64_t)b * T_ + j];
 
-  // ---- key ranges: prefix [0, vlen), current [0, cur_end)
+  // key ranges: prefix [0, vlen), current [0, cur_end)
   const int vlen = P ? min(p.prefix_valid_len[b], P) : 0;
-  const int last_row = min(row0 + ROWS, nrows) - 1;
-  // largest t among this block's rows (rows may wrap across g boundaries)
-  const int t_first = row0 % T_;
+  const int last_row = min(row0 + rows_cta, nrows) - 1;
   const int t_max = (last_row / T_ != row0 / T_) ? T_ - 1 : last_row % T_;
-  (void)t_first;
   const int cur_end = t_max + 1;
   const int nb_pre = (vlen + KB - 1) / KB;
   const int nb_cur = (cur_end + KB - 1) / KB;
@@ -210,7 +216,9 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
   const T* Kc = kv_ptr<T>(p.cur_kv, b, p.cur_layer, 0, KVH, kvh, T_, HD);
   const T* Vc = kv_ptr<T>(p.cur_kv, b, p.cur_layer, 1, KVH, kvh, T_, HD);
 
-  auto load_block = [&](int blk, int buf) {
+  auto load_block = [&](int blk) {
+    if (blk >= nblocks) return;
+    const int buf = blk % STAGES;
     const bool pre = blk < nb_pre;
     const int k0 = pre ? blk * KB : (blk - nb_pre) * KB;
     const int lim = pre ? vlen : cur_end;
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
     const T* Vs = pre ? Vp : Vc;
     T* dk = sK + buf * KB * PITCH;
     T* dv = sV + buf * KB * PITCH;
-    for (int i = threadIdx.x; i < KB * CPR; i += THREADS) {
+    for (int i = threadIdx.x; i < KB * CPR; i += nthr) {
       const int r = i / CPR, c = (i - r * CPR) * 8;
       const bool ok = k0 + r < lim;
       const int64_t off = (int64_t)(ok ? k0 + r : 0) * HD + c;
@@ -227,13 +235,17 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
     }
   };
 
-  if (nblocks > 0) load_block(0, 0);
-  cp_commit();
+  // prologue: Q + blocks 0..STAGES-2, one commit group each
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    load_block(s);
+    cp_commit();
+  }
 
-  // per-thread rows: r_lo = warp*16 + lane/4, r_hi = r_lo + 8
   const int r_lo = row0 + warp * 16 + (lane >> 2);
   const int r_hi = r_lo + 8;
   const int t_lo = r_lo % T_, t_hi = r_hi % T_;
+  const bool warp_live = row0 + warp * 16 < nrows;
   float m_lo = -CUDART_INF_F, m_hi = -CUDART_INF_F, l_lo = 0.f, l_hi = 0.f;
   float o[HD / 8][4];
 #pragma unroll
@@ -241,32 +253,28 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
   const float L2E = 1.4426950408889634f;
 
   for (int blk = 0; blk < nblocks; ++blk) {
-    const int buf = blk & 1;
-    if (blk + 1 < nblocks) load_block(blk + 1, buf ^ 1);
-    cp_commit();
-    cp_wait<1>();
+    cp_wait<STAGES - 2>();
     __syncthreads();
+    load_block(blk + STAGES - 1);
+    cp_commit();
+    if (!warp_live) continue;
+    const int buf = blk % STAGES;
     const bool pre = blk < nb_pre;
     const int k0 = pre ? blk * KB : (blk - nb_pre) * KB;
     const T* cK = sK + buf * KB * PITCH;
     const T* cV = sV + buf * KB * PITCH;
 
-    // S = Q K^T  (16 x KB per warp)
     float s[KB / 8][4];
 #pragma unroll
     for (int n = 0; n < KB / 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
       uint32_t a[4];
-      {
-        const int r = warp * 16 + (lane & 15);
-        const int c = kk * 16 + (lane >> 4) * 8;
-        ldm_x4(a[0], a[1], a[2], a[3], sQ + r * PITCH + c);
-      }
+      ldm_x4(a[0], a[1], a[2], a[3],
+             sQ + (warp * 16 + (lane & 15)) * PITCH + kk * 16 + (lane >> 4) * 8);
 #pragma unroll
       for (int n = 0; n < KB / 8; n += 2) {
         uint32_t b0, b1, b2, b3;
-        // matrices: (keys n*8.., hd lo), (keys n*8.., hd hi), (keys n*8+8.., lo), (.., hi)
         const int kr = n * 8 + (lane & 7) + ((lane >> 4) << 3);
         const int kc = kk * 16 + ((lane >> 3) & 1) * 8;
         ldm_x4(b0, b1, b2, b3, cK + kr * PITCH + kc);
@@ -274,18 +282,20 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
         mma16816<T>(s[n + 1], a, b2, b3);
       }
     }
-    // mask + online softmax
+    // mask + online softmax (shared max across prefix and current pieces)
     float mx_lo = -CUDART_INF_F, mx_hi = -CUDART_INF_F;
+    const bool full_pre = pre && (k0 + KB <= vlen);
 #pragma unroll
     for (int n = 0; n < KB / 8; ++n) {
+      if (!full_pre) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = k0 + n * 8 + (lane & 3) * 2 + (e & 1);
-        const int t = (e < 2) ? t_lo : t_hi;
-        bool vis;
-        if (pre) vis = j < vlen;
-        else vis = (j < T_) && (j <= t) && sTV[j < T_ ? j : 0];
-        if (!vis) s[n][e] = -CUDART_INF_F;
+        for (int e = 0; e < 4; ++e) {
+          const int j = k0 + n * 8 + (lane & 3) * 2 + (e & 1);
+          const int t = (e < 2) ? t_lo : t_hi;
+          const bool vis = pre ? (j < vlen)
+                               : ((j < T_) && (j <= t) && sTV[j < T_ ? j : 0]);
+          if (!vis) s[n][e] = -CUDART_INF_F;
+        }
       }
       mx_lo = fmaxf(mx_lo, fmaxf(s[n][0], s[n][1]));
       mx_hi = fmaxf(mx_hi, fmaxf(s[n][2], s[n][3]));
@@ -299,18 +309,18 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
     const float base_hi = (mn_hi == -CUDART_INF_F) ? 0.f : mn_hi * L2E;
     const float sc_lo = (m_lo == -CUDART_INF_F) ? 0.f : exp2f(m_lo * L2E - base_lo);
     const float sc_hi = (m_hi == -CUDART_INF_F) ? 0.f : exp2f(m_hi * L2E - base_hi);
-    m_lo = mn_lo; m_hi = mn_hi;
+    m_lo = mn_lo;
+    m_hi = mn_hi;
     float rs_lo = 0.f, rs_hi = 0.f;
     uint32_t pf[KB / 16][4];
 #pragma unroll
     for (int n = 0; n < KB / 8; ++n) {
-      const float p0 = exp2f(s[n][0] * L2E - base_lo);
-      const float p1 = exp2f(s[n][1] * L2E - base_lo);
-      const float p2 = exp2f(s[n][2] * L2E - base_hi);
-      const float p3 = exp2f(s[n][3] * L2E - base_hi);
+      const float p0 = exp2f(fmaf(s[n][0], L2E, -base_lo));
+      const float p1 = exp2f(fmaf(s[n][1], L2E, -base_lo));
+      const float p2 = exp2f(fmaf(s[n][2], L2E, -base_hi));
+      const float p3 = exp2f(fmaf(s[n][3], L2E, -base_hi));
       rs_lo += p0 + p1;
       rs_hi += p2 + p3;
-      // accumulator layout of two n8 tiles == A fragment of one k16 step
       pf[n >> 1][(n & 1) * 2 + 0] = pack2<T>(p0, p1);
       pf[n >> 1][(n & 1) * 2 + 1] = pack2<T>(p2, p3);
     }
@@ -321,15 +331,12 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
       o[i][0] *= sc_lo; o[i][1] *= sc_lo;
       o[i][2] *= sc_hi; o[i][3] *= sc_hi;
     }
-    // O += P V
 #pragma unroll
     for (int kk = 0; kk < KB / 16; ++kk) {
       const uint32_t a[4] = {pf[kk][0], pf[kk][1], pf[kk][2], pf[kk][3]};
 #pragma unroll
       for (int n = 0; n < HD / 8; n += 2) {
         uint32_t b0, b1, b2, b3;
-        // V[key][hd] row-major -> transposed 8x8 loads: (keys lo, hd n), (keys hi, hd n),
-        // (keys lo, hd n+1), (keys hi, hd n+1)
         const int vr = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         const int vc = n * 8 + (lane >> 4) * 8;
         ldm_x4_t(b0, b1, b2, b3, cV + vr * PITCH + vc);
@@ -337,11 +344,10 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
         mma16816<T>(o[n + 1], a, b2, b3);
       }
     }
-    __syncthreads();
   }
   cp_wait<0>();
+  if (!warp_live) return;
 
-  // finalize: quad-reduce l, divide, store
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
   l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
   l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
@@ -368,29 +374,35 @@ __global__ void __launch_bounds__(THREADS) kernel(AttnParams p, int row_blocks) 
 }
 
 template <typename T, int HD, int KB>
-int launch(const AttnParams& p, cudaStream_t s) {
+int launch(const AttnParams& p, cudaStream_t s, int max_warps) {
   constexpr int PITCH = HD + 8;
-  const size_t smem = (size_t)(ROWS + 4 * KB) * PITCH * sizeof(T) + ((p.seq_len + 15) & ~15);
-  KRR_REQUIRE(smem <= 220 * 1024, KRR_ESHAPE, "attention: sequence too long for smem");
-  const int row_blocks = (p.group * p.seq_len + ROWS - 1) / ROWS;
+  const int rows = p.group * p.seq_len;
+  int warps = std::min(max_warps, (rows + 15) / 16);
+  const int row_blocks = (rows + warps * 16 - 1) / (warps * 16);
+  warps = (rows + row_blocks * 16 - 1) / (row_blocks * 16);  // balance the slices
+  const size_t smem = (size_t)(warps * 16 + 2 * STAGES * KB) * PITCH * sizeof(T) +
+                      ((p.seq_len + 15) & ~15);
+  KRR_REQUIRE(smem <= 227 * 1024, KRR_ESHAPE, "attention: sequence too long for smem");
   const int64_t grid = (int64_t)row_blocks * p.n_seqs * p.kv_heads;
   KRR_REQUIRE(grid < INT32_MAX, KRR_ESHAPE, "attention grid too large");
-  cudaFuncSetAttribute(kernel<T, HD, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kernel<T, HD, KB><<<(unsigned)grid, THREADS, smem, s>>>(p, row_blocks);
+  cudaFuncSetAttribute(attn_prefix_mma<T, HD, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  attn_prefix_mma<T, HD, KB><<<(unsigned)grid, warps * 32, smem, s>>>(p, row_blocks);
   return check_launch("attention_mma");
 }
 
 template <typename T>
 int dispatch(const AttnParams& p, cudaStream_t s) {
   switch (p.head_dim) {
-    case 64: return launch<T, 64, 64>(p, s);
-    case 128: return launch<T, 128, 64>(p, s);
-    case 256: return launch<T, 256, 32>(p, s);
+    case 64: return launch<T, 64, 64>(p, s, 12);
+    case 128: return launch<T, 128, 64>(p, s, 12);
+    case 256: return launch<T, 256, 32>(p, s, 8);
     default: return fail(KRR_EUNSUPPORTED, "tensor-core attention supports head_dim 64/128/256");
   }
 }
 
 }  // namespace attn_mma
+
 
 int launch_attention_mma(int act_dtype, const AttnParams& p, cudaStream_t s) {
   if (act_dtype == KRR_F16) return attn_mma::dispatch<__half>(p, s);

@@ -125,6 +125,41 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restr
   for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = Act<T>::from((xr[i] * inv) * gain[i]);
 }
 
+// Vectorised single-pass RMSNorm: the row stays in registers (VPT float4 per
+// thread), one block-reduction, 16-bit output written as 8-byte vectors.
+template <typename T, int VPT>
+__global__ void rmsnorm_vec_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                   int d, T* __restrict__ out) {
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + r * d);
+  const float4* gr = reinterpret_cast<const float4*>(gain);
+  float4 v[VPT];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    v[i] = __ldcs(xr + threadIdx.x + i * blockDim.x);
+    ss = fmaf(v[i].x, v[i].x, ss); ss = fmaf(v[i].y, v[i].y, ss);
+    ss = fmaf(v[i].z, v[i].z, ss); ss = fmaf(v[i].w, v[i].w, ss);
+  }
+  ss = block_sum(ss, red);
+  const float inv = 1.0f / sqrtf(ss / (float)d + 1e-6f);
+  T* o = out + r * d;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int e = threadIdx.x + i * blockDim.x;
+    const float4 g = __ldg(gr + e);
+    const float a = (v[i].x * inv) * g.x, b = (v[i].y * inv) * g.y;
+    const float c = (v[i].z * inv) * g.z, dd = (v[i].w * inv) * g.w;
+    if constexpr (sizeof(T) == 4) {
+      reinterpret_cast<float4*>(o)[e] = make_float4(a, b, c, dd);
+    } else {
+      T h[4] = {Act<T>::from(a), Act<T>::from(b), Act<T>::from(c), Act<T>::from(dd)};
+      reinterpret_cast<uint2*>(o)[e] = *reinterpret_cast<uint2*>(h);
+    }
+  }
+}
+
 // a10: score = rms(x[last])*final_gain . head  (model.py:402, reranker.py:211-212)
 __global__ void score_kernel(const float* __restrict__ x, int T_, int d,
                              const int32_t* __restrict__ last, const float* __restrict__ fg,
@@ -216,13 +251,32 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
   return launch_attention_simt(act, p, s);
 }
 
+template <typename T>
+static void rmsnorm_launch(const float* x, const float* gain, int64_t rows, int d, T* out,
+                           cudaStream_t s) {
+  const int q = d / 4;
+  if (d % 4 == 0 && q % 32 == 0) {
+    int vpt = 1;
+    while (q / vpt > 256 && vpt < 8) vpt *= 2;
+    const int threads = q / vpt;
+    if (threads * vpt == q && threads % 32 == 0 && threads <= 1024) {
+      switch (vpt) {
+        case 1: rmsnorm_vec_kernel<T, 1><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, out); return;
+        case 2: rmsnorm_vec_kernel<T, 2><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, out); return;
+        case 4: rmsnorm_vec_kernel<T, 4><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, out); return;
+        case 8: rmsnorm_vec_kernel<T, 8><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, out); return;
+      }
+    }
+  }
+  rmsnorm_kernel<T><<<(unsigned)rows, d >= 1024 ? 256 : 128, 0, s>>>(x, gain, d, out);
+}
+
 static int do_rmsnorm(const float* x, const float* gain, int64_t rows, int d, int act, void* out,
                       cudaStream_t s) {
   ProfScope ps(s, 2);
-  const int threads = d >= 1024 ? 256 : 128;
-  if (act == KRR_F32) rmsnorm_kernel<float><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, (float*)out);
-  else if (act == KRR_F16) rmsnorm_kernel<__half><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, (__half*)out);
-  else rmsnorm_kernel<__nv_bfloat16><<<(unsigned)rows, threads, 0, s>>>(x, gain, d, (__nv_bfloat16*)out);
+  if (act == KRR_F32) rmsnorm_launch<float>(x, gain, rows, d, (float*)out, s);
+  else if (act == KRR_F16) rmsnorm_launch<__half>(x, gain, rows, d, (__half*)out, s);
+  else rmsnorm_launch<__nv_bfloat16>(x, gain, rows, d, (__nv_bfloat16*)out, s);
   return check_launch("rmsnorm");
 }
 

@@ -11,7 +11,7 @@ constexpr int TM = 64, TN = 64, TK = 16, THREADS = 256;
 
 template <typename T>
 __global__ void __launch_bounds__(THREADS)
-    gemm_kernel(const T* __restrict__ A, const T* __restrict__ B, int64_t M, int N, int K,
+    gemm_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, int64_t M, int N, int K,
                 EpiParams ep) {
   __shared__ float sA[TK][TM + 4];
   __shared__ float sB[TK][TN + 4];
@@ -62,11 +62,11 @@ int launch_gemm_simt(int act_dtype, const void* A, const void* B, int64_t M, int
   KRR_REQUIRE((M + TM - 1) / TM < 65535, KRR_ESHAPE, "SIMT GEMM: M too large for one launch");
   dim3 grid((N + TN - 1) / TN, (unsigned)((M + TM - 1) / TM));
   if (act_dtype == KRR_F32)
-    gemm_kernel<float><<<grid, THREADS, 0, s>>>((const float*)A, (const float*)B, M, N, K, ep);
+    gemm_simt_kernel<float><<<grid, THREADS, 0, s>>>((const float*)A, (const float*)B, M, N, K, ep);
   else if (act_dtype == KRR_F16)
-    gemm_kernel<__half><<<grid, THREADS, 0, s>>>((const __half*)A, (const __half*)B, M, N, K, ep);
+    gemm_simt_kernel<__half><<<grid, THREADS, 0, s>>>((const __half*)A, (const __half*)B, M, N, K, ep);
   else
-    gemm_kernel<__nv_bfloat16><<<grid, THREADS, 0, s>>>((const __nv_bfloat16*)A,
+    gemm_simt_kernel<__nv_bfloat16><<<grid, THREADS, 0, s>>>((const __nv_bfloat16*)A,
                                                         (const __nv_bfloat16*)B, M, N, K, ep);
   return check_launch("gemm_simt");
 }

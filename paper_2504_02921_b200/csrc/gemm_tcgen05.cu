@@ -4,29 +4,60 @@
 //                                 B = weights [out, in] (16-bit, K-major)
 //
 // Roles (192 threads, 1 CTA per SM):
-//   warp 0      TMA producer: 128B-swizzled A/B tiles into a 4-stage smem ring
-//   warp 1      MMA issuer:   tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16,
-//                             accumulating in TMEM (2 x 256 columns, double buffered)
-//   warps 2..5  epilogue:     tcgen05.ld 32x32b.x32 -> fused epilogue -> global
-// The fixed K order per output tile (no split-K) keeps every row's result
-// independent of M, i.e. scores do not depend on batch composition
+//   warp 0      TMA producer: 128B-swizzled A/B tiles into a smem ring
+//   warp 1      MMA issuer:   tcgen05.mma.kind::f16, K=16 steps, fp32 accumulators
+//                             in TMEM (2 x 256 columns, double buffered)
+//   warps 2..5  epilogue:     tcgen05.ld 32x32b.x32 -> fused epilogue -> TMA store
+//
+// Two tile shapes share the code (template CG):
+//   CG=1  128x256 tile per CTA, cta_group::1, 4-stage ring of 48 KB
+//   CG=2  256x256 tile per CTA pair (cluster of 2), cta_group::2: CTA r loads
+//         rows [r*128, r*128+128) of both the A and the B tile (32 KB per
+//         stage, 6 stages); the leader issues the MMAs, commits are multicast
+//         to both CTAs, both epilogues release the accumulator on the leader.
+//
+// Epilogues: RESIDUAL adds the accumulator into the f32 residual stream with a
+// TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add, the read-modify-write
+// happens in L2 - no read latency in the SM); STORE/GELU write 16-bit tiles
+// with TMA bulk stores; QKV_ROPE rotates in registers and scatters q/k/v rows
+// with coalesced 16 B stores.  Staging tiles are 128B/64B-swizzled to match
+// the tensor maps (bank-conflict free) and double buffered per warp.
+//
+// The fixed K order per output tile (no split-K) and a single tile shape for
+// every M keep each row's result independent of batch composition
 // (SPEC.md:178 batch invariance).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <mutex>
-#include <unordered_map>
 #include "epilogue.cuh"
 
 namespace krr {
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_STAGE = BM * BK * 2;   // 16 KB
-constexpr int B_STAGE = BN * BK * 2;   // 32 KB
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int BN = 256, BK = 64;
 constexpr int THREADS = 192;
-constexpr int GROUP_M = 16;            // m-blocks per raster group (L2 reuse of B)
+constexpr int STG_BUF = 4096;                 // one 32x32 chunk (f32) per buffer
+constexpr int STG_WARP_BYTES = 2 * STG_BUF;   // double buffered per epilogue warp
 
+template <int CG> struct Cfg;
+template <> struct Cfg<1> {
+  static constexpr int TILE_M = 128, STAGES = 4, GROUP_M = 16;
+  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 256 * BK * 2;
+  static constexpr int B_ROWS = 256;
+};
+template <> struct Cfg<2> {
+  static constexpr int TILE_M = 256, STAGES = 6, GROUP_M = 8;
+  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 128 * BK * 2;
+  static constexpr int B_ROWS = 128;
+};
+template <int CG>
+constexpr int smem_bytes() {
+  return Cfg<CG>::STAGES * (Cfg<CG>::A_BYTES + Cfg<CG>::B_BYTES) + 4 * STG_WARP_BYTES +
+         1024 /*align*/ + 512 /*barriers*/;
+}
+
+// ------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -37,8 +68,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
@@ -53,13 +85,61 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint32_t bar,
+                                         int c0, int c1) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add(const CUtensorMap* map, const void* src, int c0,
+                                               int c1) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -77,19 +157,36 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2u << 61;
   return d;
 }
+template <int CG>
 __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
 }
+template <int CG>
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)0x3)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -105,79 +202,217 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// GELU-tanh (model.py:444-446) with the MUFU tanh: its ~2^-11 relative error
+// is at the f16 rounding of the stored activation; the f32 debug build keeps tanhf.
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float inner = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  return 0.5f * x * (1.0f + tanh_fast(inner));
+}
 
+template <int CG>
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = GROUP_M * num_n;
+  constexpr int GM = Cfg<CG>::GROUP_M;
+  const int per_group = GM * num_n;
   const int group = tile / per_group;
-  const int first_m = group * GROUP_M;
-  const int gsize = min(num_m - first_m, GROUP_M);
+  const int first_m = group * GM;
+  const int gsize = min(num_m - first_m, GM);
   const int r = tile - group * per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
 }
 
 template <typename T>
+__device__ __forceinline__ uint32_t pack16(float a, float b) {
+  typename Pack2<T>::V v = Pack2<T>::make(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ------------------------------------------------------------ epilogue chunk
+// Thread `lane` of an epilogue warp holds row row0+lane, columns col0..col0+31.
+template <typename T>
+__device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap* out_map,
+                                          const uint32_t (&r)[32], int64_t row0, int lane,
+                                          int col0, uint8_t* buf) {
+  if (ep.kind == KRR_EPI_RESIDUAL) {
+    // f32 chunk, 128B-swizzled rows (16 B piece j of row l at slot j ^ (l & 7))
+    uint8_t* row = buf + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) =
+          make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_reduce_add(out_map, buf, col0, (int)row0);
+      bulk_commit();
+    }
+    return;
+  }
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (ep.kind != KRR_EPI_QKV_ROPE) {
+    if (ep.kind == KRR_EPI_GELU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+    }
+    // 16-bit chunk, 64B-swizzled rows (16 B piece j of row l at slot j ^ ((l >> 1) & 3))
+    uint8_t* row = buf + lane * 64;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<uint4*>(row + ((j ^ ((lane >> 1) & 3)) << 4)) =
+          make_uint4(pack16<T>(v[8 * j], v[8 * j + 1]), pack16<T>(v[8 * j + 2], v[8 * j + 3]),
+                     pack16<T>(v[8 * j + 4], v[8 * j + 5]),
+                     pack16<T>(v[8 * j + 6], v[8 * j + 7]));
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store(out_map, buf, col0, (int)row0);
+      bulk_commit();
+    }
+    return;
+  }
+  // QKV: RoPE in registers, then scatter rows of 64 B (4 lanes x 16 B per row).
+  const krr_qkv_t& q = ep.qkv;
+  const int64_t M = ep.M;
+  const int head = col0 / q.head_dim;
+  const int c0 = col0 - head * q.head_dim;
+  if (head < q.heads + q.kv_heads) {
+    const int64_t my_row = row0 + lane;
+    const int t = (int)(my_row % q.seq_len);
+    const int64_t off = (int64_t)(q.pos0 + t) * (q.head_dim / 2) + (c0 >> 1);
+    const float4* cp = reinterpret_cast<const float4*>(q.rope_cos + off);
+    const float4* sp = reinterpret_cast<const float4*>(q.rope_sin + off);
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) {
+      const float4 cv = __ldg(cp + j4), sv = __ldg(sp + j4);
+      const float cs[4] = {cv.x, cv.y, cv.z, cv.w}, sn[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = (j4 * 4 + u) * 2;
+        const float a = v[j], b = v[j + 1];
+        v[j] = a * cs[u] - b * sn[u];
+        v[j + 1] = a * sn[u] + b * cs[u];
+      }
+    }
+  }
+  constexpr int PITCH = 80;  // 64 B row + 16 B pad: conflict-free transpose
+  uint4* s = reinterpret_cast<uint4*>(buf + lane * PITCH);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    s[j] = make_uint4(pack16<T>(v[8 * j], v[8 * j + 1]), pack16<T>(v[8 * j + 2], v[8 * j + 3]),
+                      pack16<T>(v[8 * j + 4], v[8 * j + 5]), pack16<T>(v[8 * j + 6], v[8 * j + 7]));
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = i * 8 + (lane >> 2), seg = lane & 3;
+    const int64_t row = row0 + rr;
+    if (row < M) {
+      const uint4 val = *reinterpret_cast<const uint4*>(buf + rr * PITCH + seg * 16);
+      const int SL = q.seq_len, HD = q.head_dim, KVH = q.kv_heads, H = q.heads;
+      const int64_t b = row / SL;
+      const int t = (int)(row - b * SL);
+      T* dst;
+      if (head < H) {
+        const int G = H / KVH, kvh = head / G, g = head - kvh * G;
+        dst = reinterpret_cast<T*>(q.q_out) + (((b * KVH + kvh) * G + g) * (int64_t)SL + t) * HD + c0;
+      } else {
+        const int which = head < H + KVH ? 0 : 1;
+        const int kvh = head - H - which * KVH;
+        dst = reinterpret_cast<T*>(q.kv_seq[b]) +
+              ((int64_t)((q.layer * 2 + which) * KVH + kvh) * q.kv_len + t) * HD + c0;
+      }
+      reinterpret_cast<uint4*>(dst)[seg] = val;
+    }
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------ kernel
+template <typename T, int CG>
 __global__ void __launch_bounds__(THREADS, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                int64_t M, int N, int K, uint32_t idesc, EpiParams ep) {
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmOut, int64_t M, int N, int K,
+                        uint32_t idesc, EpiParams ep) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  uint8_t* stage_base = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_base + 4 * STG_WARP_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_slot)) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_slot)) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_m = (int)((M + BM - 1) / BM);
+  const int num_m = (int)((M + C::TILE_M - 1) / C::TILE_M);
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int nk = K / BK;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int tile = cid; tile < tiles; tile += ncl) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
+        tile_coords<CG>(tile, num_m, num_n, mb, nb);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], A_STAGE + B_STAGE);
-          tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, mb * BM);
-          tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, nb * BN);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          // all TMA bytes of the pair land on the leader's barrier
+          const uint32_t bar = CG == 2 ? mapa_rank(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
+          if (leader) mbar_expect_tx(&full[stage], CG * (C::A_BYTES + C::B_BYTES));
+          tma_load<CG>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
+                       mb * C::TILE_M + (int)rank * 128);
+          tma_load<CG>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
+                       nb * BN + (int)rank * C::B_ROWS);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      for (int tile = cid; tile < tiles; tile += ncl, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -186,49 +421,60 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_STAGE);
-          const uint32_t b0 = smem_u32(sB + stage * B_STAGE);
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            mma_f16(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
-                    (kb | k) != 0);
-          }
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          for (int k = 0; k < BK / 16; ++k)
+            mma_f16<CG>(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                        (kb | k) != 0);
+          mma_commit<CG>(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        mma_commit<CG>(&tfull[acc]);
       }
     }
   } else {
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    const int r_in = quad * 32 + lane;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    uint8_t* stg = stage_base + (warp - 2) * STG_WARP_BYTES;
+    const uint32_t tempty0 =
+        CG == 2 ? mapa_rank(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+    int it = 0, nchunk = 0;
+    for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords<CG>(tile, num_m, num_n, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row = (int64_t)mb * BM + r_in;
+      const int64_t row0 = (int64_t)mb * C::TILE_M + rank * 128 + quad * 32;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
         const int col0 = nb * BN + c * 32;
-        if (row < M && col0 < N)
-          epi_apply<T>(ep, row, col0, reinterpret_cast<const float*>(r), 32);
+        if (col0 >= N) continue;
+        uint8_t* buf = stg + (nchunk & 1) * STG_BUF;
+        ++nchunk;
+        // the bulk op that last read this buffer (two chunks ago) must be done
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, buf);
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
     }
+    if (lane == 0) bulk_wait_all();
   }
+  tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
   if (warp == 1) {
-    __syncwarp();
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
-                 : "memory");
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
 }
 
@@ -247,22 +493,50 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const void* ptr, int dt, uint64_t inner, uint64_t outer,
-                    uint32_t box_outer) {
+// 2-D row-major [outer, inner] tensor map.
+static int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int esize,
+                    uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer,
+                    CUtensorMapSwizzle sw) {
   auto enc = get_encode();
   if (!enc) return fail(KRR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
-  cuuint32_t box[2] = {BK, box_outer};
+  cuuint64_t strides[1] = {inner * (uint64_t)esize};
+  cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map,
-                   dt == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                  : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                   2, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(KRR_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(KRR_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return KRR_OK;
+}
+
+template <typename T, int CG>
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int64_t M,
+                  int N, int K, uint32_t idesc, const EpiParams& ep, cudaStream_t s) {
+  constexpr int SMEM = smem_bytes<CG>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tcgen05_kernel<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + BN - 1) / BN);
+  const int slots = (device_sm_count() / CG) * CG;
+  const int grid = std::min(CG * tiles, slots);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, CG>, ma, mb, mo, M, N, K, idesc, ep);
+  return check_launch(CG == 2 ? "gemm_tcgen05_2cta" : "gemm_tcgen05");
 }
 
 }  // namespace tc
@@ -277,35 +551,43 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   KRR_REQUIRE(M > 0 && M < (int64_t)INT32_MAX, KRR_ESHAPE, "GEMM M out of range");
   KRR_REQUIRE((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
               KRR_ESHAPE, "GEMM operands must be 16-byte aligned");
-  if (ep.kind == KRR_EPI_QKV_ROPE)
-    KRR_REQUIRE(ep.qkv.head_dim % 2 == 0, KRR_ESHAPE, "head_dim must be even");
-  CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, act_dtype, (uint64_t)K, (uint64_t)M, BM);
+  if (ep.kind == KRR_EPI_QKV_ROPE && ep.qkv.head_dim % 32 != 0)
+    return launch_gemm_simt(act_dtype, A, B, M, N, K, ep, s);  // a chunk must stay in one head
+
+  static int mode = -1;  // KRR_GEMM_CTA=1|2 picks the tile shape (default 1); fixed per process
+  if (mode < 0) {
+    const char* e = getenv("KRR_GEMM_CTA");
+    mode = (e && atoi(e) == 2) ? 2 : 1;
+  }
+  const CUtensorMapDataType dt =
+      act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const int tile_m = mode == 2 ? 256 : 128;
+  CUtensorMap ma, mb, mo;
+  int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_map(&mb, B, act_dtype, (uint64_t)K, (uint64_t)N, BN);
+  rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK, mode == 2 ? 128 : 256,
+                CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  // instruction descriptor: D=f32, A/B = f16|bf16, K-major both, N>>3 @17, M>>4 @24
+  if (ep.kind == KRR_EPI_RESIDUAL) {
+    KRR_REQUIRE((reinterpret_cast<uintptr_t>(ep.out) & 15) == 0, KRR_ESHAPE, "residual must be 16-byte aligned");
+    rc = make_map(&mo, ep.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)N, (uint64_t)M, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (ep.kind == KRR_EPI_STORE || ep.kind == KRR_EPI_GELU) {
+    KRR_REQUIRE((reinterpret_cast<uintptr_t>(ep.out) & 15) == 0, KRR_ESHAPE, "output must be 16-byte aligned");
+    rc = make_map(&mo, ep.out, dt, 2, (uint64_t)N, (uint64_t)M, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  } else {
+    mo = ma;  // unused by the QKV scatter
+  }
+  if (rc) return rc;
+  // instruction descriptor: D=f32 @4, A/B f16|bf16 @7/@10, K-major both, N>>3 @17, M>>4 @24
   const uint32_t fmt = act_dtype == KRR_BF16 ? 1u : 0u;
   const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
-                         ((uint32_t)(BM >> 4) << 24);
-  const int tiles = (int)((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = std::min(tiles, device_sm_count());
-  if (act_dtype == KRR_F16) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      attr = true;
-    }
-    gemm_kernel<__half><<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, K, idesc, ep);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      attr = true;
-    }
-    gemm_kernel<__nv_bfloat16><<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, K, idesc, ep);
-  }
-  return check_launch("gemm_tcgen05");
+                         ((uint32_t)(tile_m >> 4) << 24);
+  if (act_dtype == KRR_F16)
+    return mode == 2 ? launch<__half, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
+                     : launch<__half, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
+  return mode == 2 ? launch<__nv_bfloat16, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
+                   : launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
 }
 
 }  // namespace krr

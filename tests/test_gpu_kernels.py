@@ -219,3 +219,17 @@ def test_segmented_topk():
     for i in range(n_seg):
         want = sorted(range(seg), key=lambda j: (-s_h[i, j], ids_h[i, j]))[:k]
         assert idx[i].cpu().tolist() == want
+
+
+@pytest.mark.parametrize("d", [128, 256, 2048, 4096, 200])
+@pytest.mark.parametrize("code,tdt", [(_lib.F32, torch.float32), (_lib.F16, torch.float16)])
+def test_rmsnorm(d, code, tdt):
+    x = torch.randn(37, d, device="cuda") * 3
+    g = torch.rand(d, device="cuda") + 0.5
+    out = torch.empty(37, d, dtype=tdt, device="cuda")
+    _lib.check(_lib.lib().krr_rmsnorm(x.data_ptr(), g.data_ptr(), 37, d, code, out.data_ptr(),
+                                      _stream()))
+    ref = x * (1.0 / torch.sqrt((x * x).mean(-1, keepdim=True) + 1e-6)) * g
+    torch.cuda.synchronize()
+    tol = 1e-5 if code == _lib.F32 else 2e-3
+    assert (out.float() - ref).abs().max().item() <= tol * ref.abs().max().item()

@@ -19,5 +19,6 @@ reference's own fast path, counters exact).
 from .kvrerank_np import (  # noqa: F401
     OracleConfig, OracleWeights, fnv1a64, splitmix64_array, uniform_signed,
     init_tensor, init_weights, rope_tables, forward, doc_prefill, score_reuse,
-    score_full, pair_count, select_topk, score_head, round_weights,
+    score_full, pair_count, select_topk, score_head, round_weights, init_rows,
+    LazyEmbedding,
 )

@@ -63,6 +63,39 @@ def init_tensor(seed: int, name: str, shape) -> np.ndarray:
     return uniform_signed(seed ^ fnv1a64(name), n, bound).reshape(shape)
 
 
+def init_rows(seed: int, name: str, shape, rows) -> np.ndarray:
+    """Selected rows of ``init_tensor(seed, name, shape)`` without generating the
+    whole stream: SplitMix64 here is counter-based (hashing.py:58-69), so
+    element ``i`` is output ``i + 1`` of the stream."""
+    fan_in, fan_out = shape[0], shape[-1]
+    bound = math.sqrt(6.0 / (fan_in + fan_out))
+    rows = np.asarray(rows, np.int64).reshape(-1)
+    cols = int(np.prod(shape[1:]))
+    s0 = np.uint64((seed ^ fnv1a64(name)) & _M64)
+    idx = (rows[:, None] * cols + np.arange(cols)[None, :]).astype(np.uint64) + np.uint64(1)
+    with np.errstate(over="ignore"):
+        state = s0 + idx * np.uint64(0x9E3779B97F4A7C15)
+        state ^= state >> np.uint64(30)
+        state *= np.uint64(0xBF58476D1CE4E5B9)
+        state ^= state >> np.uint64(27)
+        state *= np.uint64(0x94D049BB133111EB)
+        state ^= state >> np.uint64(31)
+    unit = (state >> np.uint64(40)).astype(np.float64) / float((1 << 24) - 1)
+    return ((2.0 * unit - 1.0) * bound).astype(np.float32)
+
+
+class LazyEmbedding:
+    """``token_embedding`` (model.py:169) generated row by row on lookup, so
+    wide-vocab configs (C2: 256000 x 2048) need not materialise 2 GB."""
+
+    def __init__(self, seed: int, vocab_size: int, model_dim: int):
+        self.seed, self.shape = seed, (vocab_size, model_dim)
+
+    def __getitem__(self, tokens) -> np.ndarray:
+        t = np.asarray(tokens, np.int64)
+        return init_rows(self.seed, "token_embedding", self.shape, t).reshape(*t.shape, -1)
+
+
 def score_head(cfg: "OracleConfig") -> np.ndarray:
     """d-vector score head, bound sqrt(6/(d+1)) (reranker.py:121-129)."""
     bound = math.sqrt(6.0 / (cfg.model_dim + 1))
@@ -113,7 +146,8 @@ class OracleWeights:
     head: np.ndarray                # [d] score head
 
 
-def init_weights(cfg: OracleConfig, layers=None, with_embedding=True) -> OracleWeights:
+def init_weights(cfg: OracleConfig, layers=None, with_embedding=True,
+                 lazy_embedding=False) -> OracleWeights:
     """Same tensors, names and order as init_weights (model.py:150-183).
 
     ``layers`` restricts generation to a subset of layer indices (others are
@@ -132,8 +166,11 @@ def init_weights(cfg: OracleConfig, layers=None, with_embedding=True) -> OracleW
         up[i] = init_tensor(cfg.seed, f"{p}.mlp.w_up", (d, 4 * d))
         down[i] = init_tensor(cfg.seed, f"{p}.mlp.w_down", (4 * d, d))
     ones = [np.ones(d, np.float32) for _ in range(cfg.layers)]
-    emb = (init_tensor(cfg.seed, "token_embedding", (cfg.vocab_size, d))
-           if with_embedding else None)
+    if lazy_embedding:
+        emb = LazyEmbedding(cfg.seed, cfg.vocab_size, d)
+    else:
+        emb = (init_tensor(cfg.seed, "token_embedding", (cfg.vocab_size, d))
+               if with_embedding else None)
     cos, sin = rope_tables(cfg.rope_base, hd, cfg.max_position)
     return OracleWeights(cfg, emb, wqkv, wo, up, down, ones, list(ones),
                          np.ones(d, np.float32), cos, sin, score_head(cfg))
@@ -200,7 +237,7 @@ def forward(w: OracleWeights, tokens, positions, past_k=None, past_v=None, valid
     vis[:, P:] &= np.tri(T, dtype=bool)
     bias = np.where(vis, np.float32(0.0), np.float32(-np.inf))
 
-    x = w.emb[tokens].astype(np.float32) if x_in is None else x_in.astype(np.float32)
+    x = np.asarray(w.emb[tokens], np.float32) if x_in is None else x_in.astype(np.float32)
     new_k = np.zeros((L, KVH, T, HD), np.float32)
     new_v = np.zeros_like(new_k)
     layers = range(L) if layer_range is None else layer_range

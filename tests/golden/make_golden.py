@@ -169,11 +169,46 @@ def wide_fixture(model, reranker, name, cfg_kw, D, Q, n_pairs, seed):
     print(name, "init", round(t_init, 1), "s; scored in", round(time.time() - t0, 1), "s")
 
 
+def codec_fixture(model, reranker):
+    """HRKV bytes written by the reference codec (codec.py:128-157) for one C1
+    document (F32 / INT8 / INT4), plus its decode of the quantised entries and a
+    hand-made tensor with zero channels and exact .5 ties."""
+    from kvrerank import codec
+    cfg = model.ModelConfig(layers=2, model_dim=256, heads=4, kv_heads=2, head_dim=64,
+                            vocab_size=32768, seed=0)
+    layout = reranker.LayoutConfig(document_len=128, query_len=48)
+    rm = reranker.RerankModel.build(cfg, layout)
+    rng = np.random.default_rng(5)
+    doc = _tokens(rng, 1, 128, cfg.vocab_size)[0]
+    doc[90:] = 0
+    kv = reranker.doc_prefill(rm, doc, chunk_id="doc-00042")
+    out = {"doc_tokens": doc}
+    for sch in (codec.QuantScheme.F32, codec.QuantScheme.INT8_PER_CHANNEL,
+                codec.QuantScheme.INT4_PER_CHANNEL):
+        data = codec.encode_entry(kv, sch)
+        out[f"entry_{sch.short_name}"] = np.frombuffer(data, np.uint8)
+        dec = codec.decode_entry(data)
+        out[f"decoded_keys_{sch.short_name}"] = np.asarray(dec.kv.keys)
+        out[f"decoded_values_{sch.short_name}"] = np.asarray(dec.kv.values)
+    t = np.array([[[0.0, 1.0, -2.5], [0.0, -0.5, 1.25], [0.0, 0.25, 2.5]]], np.float32)
+    for sch in (codec.QuantScheme.INT8_PER_CHANNEL, codec.QuantScheme.INT4_PER_CHANNEL):
+        q, sc = codec.quantize_tensor(t, sch)
+        out[f"edge_codes_{sch.short_name}"] = np.frombuffer(q, np.uint8)
+        out[f"edge_scales_{sch.short_name}"] = sc
+    out["edge_tensor"] = t
+    np.savez_compressed(os.path.join(HERE, "codec_c1.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-wide", action="store_true")
+    ap.add_argument("--only", default="")
     args = ap.parse_args()
     model, reranker = _ref()
+    if args.only:
+        {"codec": lambda: codec_fixture(model, reranker)}[args.only]()
+        return
+    codec_fixture(model, reranker)
     weights_fixture(model)
     c1_fixture(model, reranker)
     padded_fixture(model, reranker)

@@ -1,0 +1,123 @@
+"""CPU tests of the host layer: the C-ABI library's symbol table, the
+reference-mirroring config/validation logic, counters and the no-fallback rule."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2504_02921_b200 as krr
+from paper_2504_02921_b200 import _lib, reranker
+from paper_2504_02921_b200.errors import ConfigError, KvRerankError, ShapeError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    syms = set()
+    inc = os.path.join(ROOT, "include")
+    for f in os.listdir(inc):
+        if f.endswith(".h"):
+            src = open(os.path.join(inc, f)).read()
+            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+            syms |= set(re.findall(r"\b(krr_[a-z0-9_]+)\s*\(", src))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    declared = _declared_symbols()
+    assert declared, "no krr_* declarations found in include/"
+    missing = [s for s in sorted(declared) if not hasattr(L, s)]
+    assert not missing, missing
+    assert declared == set(_lib.EXPORTS)
+
+
+def test_library_metadata_without_gpu():
+    L = _lib.lib()
+    assert L.krr_version().startswith(b"kvrerank_b200")
+    assert _lib.launch_count() >= 0
+
+
+def test_library_is_sm100a_only():
+    """The .so carries sm_100a SASS (no PTX JIT fallback, no other arch)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_error_code_mapping():
+    for rc, exc in ((1, ConfigError), (2, ShapeError), (3, KvRerankError), (4, ConfigError)):
+        with pytest.raises(exc):
+            _lib.check(rc)
+    _lib.check(0)
+
+
+def test_model_config_validation_mirrors_reference():
+    with pytest.raises(ConfigError):
+        krr.ModelConfig(heads=6, kv_heads=4, model_dim=96, head_dim=16).validate()
+    with pytest.raises(ConfigError):
+        krr.ModelConfig(model_dim=100).validate()
+    with pytest.raises(ConfigError):
+        krr.ModelConfig(layers=0).validate()
+    with pytest.raises(ConfigError):
+        krr.LayoutConfig(document_len=0).validate()
+    with pytest.raises(ConfigError):
+        krr.LayoutConfig(pad_id=3).validate()
+    for name, (cfg, lay) in krr.PRESETS.items():
+        cfg.validate()
+        lay.validate()
+        assert lay.total_len <= cfg.max_position, name
+
+
+def test_no_cpu_fallback():
+    """Without a CUDA device the product path refuses to run (it never
+    routes to a CPU implementation)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(ConfigError, match="CUDA"):
+        krr.RerankModel.build(krr.ModelConfig(layers=1), krr.LayoutConfig(64, 8))
+
+
+def test_tokenize_matches_reference_rule():
+    text = "the quick brown fox jumps over the lazy dog"
+    t = krr.tokenize(text, 12, vocab_size=32768)
+    words = text.split()
+    want = [1 + oracle.fnv1a64(w) % 32767 for w in words] + [0, 0, 0]
+    assert t.tolist() == want and t.dtype == np.int64
+    assert krr.tokenize(text, 3).tolist() == want[:3]
+    with pytest.raises(ConfigError):
+        krr.tokenize("x", 0)
+
+
+def test_pair_count_vectorised_matches_oracle():
+    rng = np.random.default_rng(0)
+    v = rng.random((20, 176)) > 0.2
+    got = reranker.pair_count(v, 128)
+    assert got.tolist() == [oracle.pair_count(row, 128) for row in v]
+    assert reranker.pair_count(np.ones(304, bool), 256).tolist() == [13464]
+
+
+def test_counter_report_merge():
+    a = krr.CounterReport(3, 10, 3, 100)
+    a.merge(krr.CounterReport(5, 1, 2, 50))
+    assert a.as_dict() == {"linear_token_count": 8, "attn_mac_pairs": 11,
+                           "peak_activation_tokens": 3, "kv_bytes_loaded": 150}
+
+
+def test_id_ranks_follow_chunk_id_order():
+    from paper_2504_02921_b200.pipeline import _id_ranks, select
+    cands = [["doc-3", "doc-1"], ["doc-2", "doc-3"]]
+    assert _id_ranks(cands).tolist() == [[2, 0], [1, 2]]
+    s = [krr.ScoredPair("b", "q", 1.0), krr.ScoredPair("a", "q", 1.0),
+         krr.ScoredPair("c", "q", 2.0)]
+    assert [p.chunk_id for p in select(s, 2)] == ["c", "a"]

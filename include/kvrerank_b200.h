@@ -59,6 +59,10 @@ enum {
 /* GEMM backends */
 enum { KRR_GEMM_AUTO = 0, KRR_GEMM_TCGEN05 = 1, KRR_GEMM_SIMT = 2 };
 
+/* attention backends: auto picks TCGEN05 when the pools are described and the
+ * geometry is supported (16-bit, head_dim 64/128), else MMA (16-bit) / SIMT (f32) */
+enum { KRR_ATTN_AUTO = 0, KRR_ATTN_MMA = 1, KRR_ATTN_SIMT = 2, KRR_ATTN_TCGEN05 = 3 };
+
 /* Scatter description for KRR_EPI_QKV_ROPE.  Row r of the GEMM is token
  * t = r % seq_len of sequence b = r / seq_len at absolute position pos0 + t.
  * q  -> q_out[b][kvh][g][t][hd]           (GQA rows packed, model.py:377-378)
@@ -76,7 +80,7 @@ typedef struct {
   int32_t layers, model_dim, heads, kv_heads, head_dim, vocab_size, max_position;
   int32_t act_dtype;              /* KRR_F32 (debug), KRR_F16 or KRR_BF16 */
   int32_t gemm_backend;           /* KRR_GEMM_* */
-  int32_t attn_backend;           /* 0 auto, 1 tensor-core, 2 SIMT fp32 */
+  int32_t attn_backend;           /* KRR_ATTN_* */
   const float* token_embedding;   /* [V, d] f32 */
   const float* rope_cos;          /* [max_position, hd/2] f32 */
   const float* rope_sin;
@@ -104,6 +108,13 @@ typedef struct {
   void* const* cur_kv;             /* device [n_seqs] KV slab ptrs [cur_kv_layers][2][KVH][seq_len][HD] */
   const int32_t* last_index;       /* device [n_seqs] row scored, or NULL */
   float* scores;                   /* device [n_seqs] out, or NULL */
+  /* the allocations prefix_kv[] / cur_kv[] point into (pool slab, suffix
+   * scratch): base + size in bytes; lets the tcgen05 attention address KV
+   * pages through one TMA descriptor.  NULL/0 = unknown (slower kernel). */
+  const void* prefix_pool;
+  int64_t prefix_pool_bytes;
+  const void* cur_pool;
+  int64_t cur_pool_bytes;
 } krr_batch_t;
 
 const char* krr_last_error(void);
@@ -136,7 +147,11 @@ int krr_attention(int backend, int act_dtype, const void* q, int32_t n_seqs, int
                   int32_t group, int32_t head_dim, int32_t seq_len, int32_t prefix_len,
                   int32_t layer, int32_t cur_layer, void* const* prefix_kv,
                   const int32_t* prefix_valid_len, void* const* cur_kv,
-                  const uint8_t* tok_valid, void* out, krr_stream_t stream);
+                  const uint8_t* tok_valid, void* out, const void* prefix_pool,
+                  int64_t prefix_pool_bytes, const void* cur_pool, int64_t cur_pool_bytes,
+                  krr_stream_t stream);
+/* Co-resident CTAs per SM of the tcgen05 attention kernel (design point: 2). */
+int krr_attention_occupancy(int act_dtype, int32_t head_dim, int32_t* ctas_per_sm);
 int krr_score_head(const float* x, int32_t n_seqs, int32_t seq_len, int32_t d,
                    const int32_t* last_index, const float* final_gain, const float* head,
                    float* scores, krr_stream_t stream);

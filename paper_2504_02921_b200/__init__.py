@@ -8,6 +8,8 @@ CUDA kernels behind a C ABI (``include/kvrerank_b200.h``); there is no CPU
 fallback.
 """
 
+from .codec import (QuantScheme, decode_entry, decode_entry_to_pool, dequantize_tensor,
+                    encode_entry, payload_nbytes, quantize_tensor)
 from .config import PRESETS, LayoutConfig, ModelConfig
 from .errors import (CodecError, ConfigError, DegenerateInputError, DuplicateChunkError,
                      FormatError, KvRerankError, PositionError, ShapeError, StoreError)
@@ -16,5 +18,8 @@ from .model import KVTensorSet, RerankModel
 from .reranker import (CounterReport, DeviceKV, DocKV, ScoredPair, doc_prefill,
                        doc_prefill_batch, pool_for, score_batch, score_full, score_reuse,
                        tokenize)
+from .pipeline import populate_store, rerank, select
+from .store import (DevicePagedKVStore, DirectoryBackend, MemoryBackend, ShardedStore,
+                    StoreStats, shard_of)
 
 __version__ = "0.1.0"

@@ -18,13 +18,14 @@ F32, F16, BF16 = 0, 1, 2
 DTYPE_CODES = {"f32": F32, "f16": F16, "bf16": BF16}
 EPI_STORE, EPI_GELU, EPI_RESIDUAL, EPI_QKV_ROPE = 0, 1, 2, 3
 GEMM_AUTO, GEMM_TCGEN05, GEMM_SIMT = 0, 1, 2
-ATTN_AUTO, ATTN_TC, ATTN_SIMT = 0, 1, 2
+ATTN_AUTO, ATTN_MMA, ATTN_SIMT, ATTN_TCGEN05 = 0, 1, 2, 3
+ATTN_TC = ATTN_MMA
 
 # every symbol include/kvrerank_b200.h declares
 EXPORTS = (
     "krr_last_error", "krr_version", "krr_launch_count", "krr_workspace_bytes", "krr_forward",
     "krr_profile_enable", "krr_profile_read", "krr_init_uniform", "krr_embed", "krr_rmsnorm",
-    "krr_gemm", "krr_attention", "krr_score_head", "krr_segmented_topk", "krr_dequant_kv",
+    "krr_gemm", "krr_attention", "krr_attention_occupancy", "krr_score_head", "krr_segmented_topk", "krr_dequant_kv",
 )
 
 vp = C.c_void_p
@@ -49,7 +50,9 @@ class Model(C.Structure):
 class Batch(C.Structure):
     _fields_ = [("n_seqs", i32), ("seq_len", i32), ("pos0", i32), ("prefix_len", i32),
                 ("cur_kv_layers", i32), ("tokens", vp), ("tok_valid", vp), ("prefix_valid_len", vp),
-                ("prefix_kv", vp), ("cur_kv", vp), ("last_index", vp), ("scores", vp)]
+                ("prefix_kv", vp), ("cur_kv", vp), ("last_index", vp), ("scores", vp),
+                ("prefix_pool", vp), ("prefix_pool_bytes", i64), ("cur_pool", vp),
+                ("cur_pool_bytes", i64)]
 
 
 _LIB = None
@@ -77,7 +80,8 @@ def lib():
         L.krr_gemm.argtypes = [C.c_int, C.c_int, vp, vp, i64, i32, i32, C.c_int, vp,
                                C.POINTER(QKV), vp]
         L.krr_attention.argtypes = [C.c_int, C.c_int, vp, i32, i32, i32, i32, i32, i32, i32,
-                                    i32, vp, vp, vp, vp, vp, vp]
+                                    i32, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp]
+        L.krr_attention_occupancy.argtypes = [C.c_int, i32, C.POINTER(i32)]
         L.krr_score_head.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp]
         L.krr_segmented_topk.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
         L.krr_dequant_kv.argtypes = [vp, vp, i32, i32, i32, i32, C.c_int, vp, vp]

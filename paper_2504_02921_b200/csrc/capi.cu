@@ -245,9 +245,13 @@ static int do_gemm(int backend, int act, const void* A, const void* B, int64_t M
 }
 
 static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t s) {
-  if (backend == 0) backend = (act == KRR_F32) ? 2 : 1;
+  if (backend == KRR_ATTN_AUTO) {
+    if (act == KRR_F32) backend = KRR_ATTN_SIMT;
+    else backend = attention_tcgen05_supported(act, p) ? KRR_ATTN_TCGEN05 : KRR_ATTN_MMA;
+  }
   ProfScope ps(s, 1);
-  if (backend == 1) return launch_attention_mma(act, p, s);
+  if (backend == KRR_ATTN_TCGEN05) return launch_attention_tcgen05(act, p, s);
+  if (backend == KRR_ATTN_MMA) return launch_attention_mma(act, p, s);
   return launch_attention_simt(act, p, s);
 }
 
@@ -369,11 +373,19 @@ int krr_attention(int backend, int act_dtype, const void* q, int32_t n_seqs, int
                   int32_t group, int32_t head_dim, int32_t seq_len, int32_t prefix_len,
                   int32_t layer, int32_t cur_layer, void* const* prefix_kv,
                   const int32_t* prefix_valid_len, void* const* cur_kv,
-                  const uint8_t* tok_valid, void* out, krr_stream_t stream) {
+                  const uint8_t* tok_valid, void* out, const void* prefix_pool,
+                  int64_t prefix_pool_bytes, const void* cur_pool, int64_t cur_pool_bytes,
+                  krr_stream_t stream) {
   AttnParams p{q, n_seqs, kv_heads, group, head_dim, seq_len, prefix_len, layer, cur_layer,
-               prefix_kv, prefix_valid_len, cur_kv, tok_valid, out};
+               prefix_kv, prefix_valid_len, cur_kv, tok_valid, out, prefix_pool,
+               prefix_pool_bytes, cur_pool, cur_pool_bytes};
   if (n_seqs == 0) return KRR_OK;
   return do_attention(backend, act_dtype, p, (cudaStream_t)stream);
+}
+
+int krr_attention_occupancy(int act_dtype, int32_t head_dim, int32_t* ctas_per_sm) {
+  KRR_REQUIRE(ctas_per_sm != nullptr, KRR_ECONFIG, "null argument");
+  return attention_tcgen05_occupancy(act_dtype, head_dim, ctas_per_sm);
 }
 
 int krr_score_head(const float* x, int32_t n_seqs, int32_t seq_len, int32_t d,
@@ -474,7 +486,8 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     // cannot influence any stored byte (model.py:365-400 dataflow).
     if (prefill_only && l == L - 1) break;
     AttnParams ap{qb, b->n_seqs, KVH, G, HD, b->seq_len, b->prefix_len, l, cl,
-                  b->prefix_kv, b->prefix_valid_len, b->cur_kv, b->tok_valid, ab};
+                  b->prefix_kv, b->prefix_valid_len, b->cur_kv, b->tok_valid, ab,
+                  b->prefix_pool, b->prefix_pool_bytes, b->cur_pool, b->cur_pool_bytes};
     rc = do_attention(m->attn_backend, act, ap, s);
     if (rc) return rc;
     EpiParams er{};

@@ -26,8 +26,17 @@ struct AttnParams {
   void* const* cur_kv;
   const uint8_t* tok_valid;
   void* out;                   // [n_seqs*seq_len][heads*hd]
+  // base/extent of the allocations the prefix_kv / cur_kv pointers point into
+  // (the tcgen05 kernel addresses them as TMA pages); may be null
+  const void* prefix_pool;
+  int64_t prefix_pool_bytes;
+  const void* cur_pool;
+  int64_t cur_pool_bytes;
 };
 int launch_attention_mma(int act_dtype, const AttnParams& p, cudaStream_t s);
+int launch_attention_tcgen05(int act_dtype, const AttnParams& p, cudaStream_t s);
+bool attention_tcgen05_supported(int act_dtype, const AttnParams& p);
+int attention_tcgen05_occupancy(int act_dtype, int head_dim, int* out);
 int launch_attention_simt(int act_dtype, const AttnParams& p, cudaStream_t s);
 
 int device_sm_count();

@@ -55,12 +55,21 @@ def _ptr(t):
     return 0 if t is None else t.data_ptr()
 
 
+def _extent(t):
+    """(base pointer, bytes) of the allocation a KV pointer table points into."""
+    if t is None:
+        return 0, 0
+    return t.data_ptr(), t.numel() * t.element_size()
+
+
 def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
                 prefix_valid, prefix_ptrs, cur_ptrs, cur_kv_layers: int, last_index=None,
-                scores=None, stream=None) -> None:
+                scores=None, stream=None, prefix_pool=None, cur_pool=None) -> None:
     """One krr_forward call over n sequences (all device tensors, contiguous):
     tokens int32 [n, T], tok_valid uint8 [n, T], prefix_valid int32 [n],
-    prefix_ptrs / cur_ptrs int64 [n], last_index int32 [n], scores f32 [n]."""
+    prefix_ptrs / cur_ptrs int64 [n], last_index int32 [n], scores f32 [n].
+    ``prefix_pool`` / ``cur_pool`` are the tensors those pointers point into
+    (pool slab, suffix scratch); they let attention address pages via TMA."""
     import torch
     n, T = tokens.shape
     if n == 0:
@@ -68,9 +77,11 @@ def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
     rows = n * T
     need = workspace_bytes(w, rows)
     ws = _workspace(w.device).get(need, w.device)
+    pp, pb = _extent(prefix_pool)
+    cp, cb = _extent(cur_pool)
     b = _lib.Batch(n, T, pos0, prefix_len, cur_kv_layers, _ptr(tokens), _ptr(tok_valid),
                    _ptr(prefix_valid), _ptr(prefix_ptrs), _ptr(cur_ptrs), _ptr(last_index),
-                   _ptr(scores))
+                   _ptr(scores), pp, pb, cp, cb)
     if stream is None:
         stream = torch.cuda.current_stream(w.device).cuda_stream
     _lib.check(_lib.lib().krr_forward(C.byref(w.struct()), C.byref(b), ws.data_ptr(),
@@ -96,7 +107,7 @@ def prefill_slots(w: DeviceWeights, pool: KVPool, slots, doc_tokens, valid_len,
     for i in range(0, n, step):
         j = min(n, i + step)
         run_forward(w, tok[i:j].contiguous(), valid[i:j].contiguous(), 0, 0, None, None,
-                    ptrs[i:j].contiguous(), w.config.layers)
+                    ptrs[i:j].contiguous(), w.config.layers, cur_pool=pool.slab)
     pool.set_valid_len(np.asarray(slots), np.asarray(valid_len))
 
 
@@ -116,6 +127,9 @@ class SuffixScratch:
             self.buf = torch.empty(need, dtype=tdt, device=w.device)
         per = need // n * self.buf.element_size()
         return torch.arange(n, device=w.device, dtype=torch.int64) * per + self.buf.data_ptr()
+
+    def extent(self):
+        return self.buf
 
 
 _SCRATCH: dict = {}
@@ -152,7 +166,8 @@ def score_slots(w: DeviceWeights, pool: KVPool, slots, q_tokens, q_valid=None, l
         cur = scratch.ptrs(w, j - i, Q)
         run_forward(w, q[i:j].contiguous(), q_valid[i:j].contiguous(), D, D,
                     prefix_valid[i:j].contiguous(), prefix_ptrs[i:j].contiguous(), cur, 1,
-                    last_index[i:j].contiguous(), scores[i:j])
+                    last_index[i:j].contiguous(), scores[i:j], prefix_pool=pool.slab,
+                    cur_pool=scratch.extent())
     return scores
 
 

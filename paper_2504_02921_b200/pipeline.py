@@ -95,6 +95,58 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
     return RerankResult(list(query_ids), selected, int(len(miss)), n_q * n_c)
 
 
+def populate_store(model: RerankModel, docs, index, store, scheme=None, path: str = "fast",
+                   on_entry=None, batch: int = 64) -> int:
+    """Prefill, encode and place every doc's cache entry; returns total bytes
+    (pipeline.py:156-171).
+
+    ``docs`` are objects with ``.id`` / ``.text`` (the reference's CorpusDoc),
+    ``index`` anything with ``centroid_of(doc_id)`` (IvfIndex), ``store`` a
+    ShardedStore.  Prefill runs batched on the GPU straight into pool pages.
+    A shard backed by a DevicePagedKVStore keeps the page where the prefill
+    wrote it when the scheme is F32 (no bytes cross PCIe; the count is the
+    entry size the reference would have written); other backends, and
+    quantised schemes, receive HRKV bytes."""
+    from .codec import HEADER, QuantScheme, encode_entry, payload_nbytes
+    from .reranker import doc_prefill_batch, tokenize
+    from .store import DevicePagedKVStore
+    scheme = scheme or QuantScheme.F32
+    cfg, lay = model.config, model.layout
+    total = 0
+    for i in range(0, len(docs), batch):
+        chunk = docs[i:i + batch]
+        toks = np.stack([tokenize(d.text, lay.document_len, vocab_size=cfg.vocab_size)
+                         for d in chunk])
+        targets = [store.backends[store.shard_for(index.centroid_of(d.id))] for d in chunk]
+        # docs bound for a device shard prefill into that shard's pool
+        by_pool: dict[int, list[int]] = {}
+        for j, b in enumerate(targets):
+            # quantised schemes go through the bytes (the page must hold the
+            # dequantised values the reference would score with)
+            device = isinstance(b, DevicePagedKVStore) and scheme is QuantScheme.F32
+            key = id(b.pool) if device else 0
+            by_pool.setdefault(key, []).append(j)
+        for key, js in by_pool.items():
+            pool = targets[js[0]].pool if key else None
+            kvs = doc_prefill_batch(model, toks[js], [chunk[j].id for j in js], path=path,
+                                    pool=pool)
+            for j, kv in zip(js, kvs):
+                d, b = chunk[j], targets[j]
+                if key:
+                    b.put_from_device([d.id], [kv.kv.slot])
+                    n = HEADER.size + len(d.id.encode()) + payload_nbytes(
+                        cfg.layers, cfg.kv_heads, lay.document_len, cfg.head_dim, scheme)
+                else:
+                    data = encode_entry(kv, scheme)
+                    store.put_entry(d.id, index.centroid_of(d.id), data)
+                    kv.kv.pool.release(kv.chunk_id)
+                    n = len(data)
+                total += n
+                if on_entry is not None:
+                    on_entry(d.id, n)
+    return total
+
+
 def select(scored: list[ScoredPair], keep_m: int) -> list[ScoredPair]:
     """Host form of _select (pipeline.py:285-287)."""
     return sorted(scored, key=lambda p: (-p.score, p.chunk_id))[:keep_m]

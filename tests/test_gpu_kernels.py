@@ -163,16 +163,25 @@ def _attn_ref(q, kp, vp, vlen, kc, vc, tv, G, T):
     return (e @ torch.cat([vp, vc], dim=0)) / z
 
 
-@pytest.mark.parametrize("HD,G,KVH,P,T", [(64, 2, 2, 128, 48), (128, 4, 2, 512, 48),
-                                          (256, 8, 1, 512, 48), (64, 2, 2, 0, 128),
-                                          (128, 4, 2, 0, 100)])
-@pytest.mark.parametrize("backend,act", [(_lib.ATTN_TC, _lib.F16), (_lib.ATTN_SIMT, _lib.F32),
-                                         (_lib.ATTN_TC, _lib.BF16)])
-def test_attention(HD, G, KVH, P, T, backend, act):
+ATTN_CASES = [(64, 2, 2, 128, 48, 1.0), (128, 4, 2, 512, 48, 1.0), (256, 8, 1, 512, 48, 1.0),
+              (64, 2, 2, 0, 128, 1.0), (128, 4, 2, 0, 100, 1.0), (128, 4, 2, 512, 48, 8.0),
+              (128, 4, 2, 2048, 16, 8.0), (128, 4, 2, 0, 512, 4.0), (64, 2, 2, 200, 48, 4.0)]
+
+
+@pytest.mark.parametrize("HD,G,KVH,P,T,boost", ATTN_CASES)
+@pytest.mark.parametrize("backend,act", [(_lib.ATTN_MMA, _lib.F16), (_lib.ATTN_SIMT, _lib.F32),
+                                         (_lib.ATTN_MMA, _lib.BF16),
+                                         (_lib.ATTN_TCGEN05, _lib.F16),
+                                         (_lib.ATTN_TCGEN05, _lib.BF16)])
+def test_attention(HD, G, KVH, P, T, boost, backend, act):
+    """``boost`` scales q so logits reach the magnitudes of the unscaled model
+    (std ~ sqrt(HD)), which exercises the lazy-rescale path of the tcgen05 kernel."""
+    if backend == _lib.ATTN_TCGEN05 and HD not in (64, 128):
+        pytest.skip("tcgen05 attention covers head_dim 64/128")
     nseq, L, layer = 3, 2, 1
     tdt = {_lib.F16: torch.float16, _lib.F32: torch.float32, _lib.BF16: torch.bfloat16}[act]
     sc = 1.0 / math.sqrt(math.sqrt(HD))
-    q = (torch.randn(nseq * KVH, G * T, HD, device="cuda") * sc).to(tdt)
+    q = (torch.randn(nseq * KVH, G * T, HD, device="cuda") * sc * boost).to(tdt)
     pre = (torch.randn(nseq, L, 2, KVH, max(P, 1), HD, device="cuda") * sc).to(tdt)
     cur = (torch.randn(nseq, 1, 2, KVH, T, HD, device="cuda") * sc).to(tdt)
     vlen = torch.tensor([P, max(1, P // 3), max(1, P - 7)][:nseq], dtype=torch.int32,
@@ -181,6 +190,8 @@ def test_attention(HD, G, KVH, P, T, backend, act):
     tv[1, T - 5:] = 0
     tv[2, 3] = 0
     tv[2, 10] = 0
+    if P == 0:
+        tv[0, 0] = 0          # row t=0 of seq 0 sees no key at all -> zeros
     es = pre.element_size()
     pptr = torch.arange(nseq, device="cuda", dtype=torch.int64) * (pre[0].numel() * es) + \
         pre.data_ptr()
@@ -191,7 +202,8 @@ def test_attention(HD, G, KVH, P, T, backend, act):
     _lib.check(_lib.lib().krr_attention(backend, act, q.data_ptr(), nseq, KVH, G, HD, T, P,
                                         layer, 0, pptr.data_ptr(), vlen.data_ptr(),
                                         cptr.data_ptr(), tv.data_ptr(), out.data_ptr(),
-                                        _stream()))
+                                        pre.data_ptr(), pre.numel() * es, cur.data_ptr(),
+                                        cur.numel() * es, _stream()))
     torch.cuda.synchronize()
     tol = {_lib.F16: 2e-2, _lib.BF16: 6e-2, _lib.F32: 1e-4}[act]
     for b in range(nseq):
@@ -201,8 +213,19 @@ def test_attention(HD, G, KVH, P, T, backend, act):
             ref = _attn_ref(q[b * KVH + kh].float(), kp, vp, int(vlen[b]) if P else 0,
                             cur[b, 0, 0, kh].float(), cur[b, 0, 1, kh].float(), tv[b], G, T)
             got = out.view(nseq, T, KVH, G, HD)[b, :, kh].permute(1, 0, 2).reshape(G * T, HD)
+            assert torch.isfinite(got.float()).all()
             err = (got.float() - ref).abs().max().item()
             assert err <= tol * max(1.0, ref.abs().max().item()), (b, kh, err)
+
+
+@pytest.mark.xfail(reason="cudaOccupancy reports 1 while ncu measures 2 resident CTAs "
+                          "(launch__occupancy_limit_shared_mem = 2, profiles/)", strict=False)
+def test_attention_tcgen05_two_ctas_per_sm():
+    """The tcgen05 attention is sized for two co-resident CTAs per SM."""
+    from paper_2504_02921_b200 import _lib as L
+    n = C.c_int32()
+    _lib.check(L.lib().krr_attention_occupancy(_lib.F16, 128, C.byref(n)))
+    assert n.value >= 2, n.value
 
 
 def test_segmented_topk():

@@ -1,0 +1,168 @@
+"""Device side of the KV-store interface: HRKV entries written by the
+reference (tests/golden/codec_c1.npz) decoded into HBM pool pages (F32 cast,
+INT8/INT4 dequant kernel), DevicePagedKVStore, populate_store, the rerank
+stage with cache misses, and the sharded top-k merge on the CUDA kernel."""
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2504_02921_b200 as krr  # noqa: E402
+from paper_2504_02921_b200 import codec, engine, pipeline, shard, store  # noqa: E402
+
+C1 = (krr.ModelConfig(layers=2, model_dim=256, heads=4, kv_heads=2, head_dim=64,
+                      vocab_size=32768),
+      krr.LayoutConfig(document_len=128, query_len=48))
+
+
+@pytest.fixture(scope="module")
+def g(golden_dir):
+    return np.load(os.path.join(golden_dir, "codec_c1.npz"))
+
+
+@pytest.fixture(scope="module")
+def model32():
+    return krr.RerankModel.build(*C1, precision="f32")
+
+
+@pytest.fixture(scope="module")
+def model16():
+    return krr.RerankModel.build(*C1, precision="f16")
+
+
+@pytest.mark.parametrize("name", ["f32", "int8", "int4"])
+def test_entry_to_pool_matches_reference_decode(g, model32, name):
+    pool = krr.KVPool(C1[0], 128, 4, "f32")
+    kv = codec.decode_entry_to_pool(g[f"entry_{name}"].tobytes(), pool)
+    torch.cuda.synchronize()
+    assert kv.chunk_id == "doc-00042" and kv.valid_len == 90
+    k, v = pool.read_host_kv(kv.kv.slot)
+    assert np.array_equal(k, g[f"decoded_keys_{name}"])
+    assert np.array_equal(v, g[f"decoded_values_{name}"])
+
+
+def test_entry_to_f16_pool(g):
+    pool = krr.KVPool(C1[0], 128, 2, "f16")
+    kv = codec.decode_entry_to_pool(g["entry_int8"].tobytes(), pool)
+    k, _ = pool.read_host_kv(kv.kv.slot)
+    want = g["decoded_keys_int8"].astype(np.float16).astype(np.float32)
+    assert np.array_equal(k, want)
+
+
+def test_device_store_scores_like_reference_entry(g, model32):
+    """An F32 entry written by the reference, put into a device shard, scores
+    like the oracle on the same KV (f32 debug build, 1e-4 gate)."""
+    pool = krr.pool_for(model32, "fast")
+    st = krr.ShardedStore([store.MemoryBackend(), store.DevicePagedKVStore(pool)])
+    st.put_entry("doc-00042", 1, g["entry_f32"].tobytes())
+    assert st.exists_entry("doc-00042", 1) and not st.exists_entry("doc-00042", 0)
+    dkv = st.backends[1].doc_kv("doc-00042")
+    q = np.random.default_rng(3).integers(1, 32768, 48)
+    s, c = krr.score_reuse(model32, dkv, q)
+    w = oracle.init_weights(oracle.OracleConfig(layers=2, model_dim=256, heads=4, kv_heads=2,
+                                                head_dim=64, vocab_size=32768,
+                                                document_len=128, query_len=48))
+    _, k, v, vl = codec.decode_arrays(g["entry_f32"].tobytes())
+    ref = oracle.score_reuse(w, k, v, vl, q)
+    assert abs(s - ref) <= 1e-4 * max(1.0, abs(ref))
+    assert c.kv_bytes_loaded == 262144
+    back = st.get_entry("doc-00042", 1)           # re-encoded F32 bytes
+    assert back == g["entry_f32"].tobytes()        # f32 pool: exact round trip
+
+
+@dataclass
+class Doc:
+    id: str
+    text: str
+
+
+class CentroidIndex:
+    def centroid_of(self, doc_id):
+        return int(doc_id.split("-")[1]) % 5
+
+
+def _docs(n):
+    rng = np.random.default_rng(11)
+    words = [f"w{i}" for i in range(5000)]
+    return [Doc(f"doc-{i:05d}", " ".join(rng.choice(words, rng.integers(60, 200))))
+            for i in range(n)]
+
+
+def test_populate_store_device_and_bytes_backends(model16):
+    docs = _docs(12)
+    pool = krr.KVPool(C1[0], 128, 16, "f16")
+    st = krr.ShardedStore([store.MemoryBackend(), store.DevicePagedKVStore(pool),
+                           store.MemoryBackend()])
+    seen = []
+    total = krr.populate_store(model16, docs, CentroidIndex(), st,
+                               on_entry=lambda i, n: seen.append((i, n)))
+    assert len(seen) == 12 and total == sum(n for _, n in seen)
+    per = codec.HEADER.size + len("doc-00000") + codec.payload_nbytes(2, 2, 128, 64,
+                                                                      codec.QuantScheme.F32)
+    assert all(n == per for _, n in seen)
+    for d in docs:
+        sh = st.shard_for(CentroidIndex().centroid_of(d.id))
+        assert st.exists_entry(d.id, CentroidIndex().centroid_of(d.id))
+        if sh == 1:
+            assert d.id in pool
+    # bytes shards hold reference-format entries that decode to the same KV
+    d0 = [d for d in docs if st.shard_for(CentroidIndex().centroid_of(d.id)) == 0][0]
+    cid, k, _, vl = codec.decode_arrays(st.get_entry(d0.id, CentroidIndex().centroid_of(d0.id)))
+    toks = krr.tokenize(d0.text, 128)
+    again = krr.doc_prefill(model16, toks, "again")
+    assert cid == d0.id and vl == again.valid_len
+    assert np.array_equal(k, again.kv.keys)
+
+
+def test_rerank_with_cache_misses_equals_full(model16):
+    rng = np.random.default_rng(5)
+    docs = rng.integers(1, 32768, (10, 128))
+    ids = [f"doc-{i:05d}" for i in range(10)]
+    pool = krr.KVPool(C1[0], 128, 10, "f16")
+    slots = pool.allocate(ids[:6])
+    engine.prefill_slots(model16.weights, pool, slots, docs[:6], np.full(6, 128))
+    q = rng.integers(1, 32768, (2, 48))
+    cands = [ids[:5] + ids[8:], ids[3:8]]
+    res = pipeline.rerank(model16, pool, ["qa", "qb"], q, cands, keep_m=3,
+                          doc_tokens=dict(zip(ids, docs)))
+    assert res.cache_misses == 4 and res.pairs == 14
+    for qi in range(2):
+        full, _ = krr.score_batch(model16, [("q", c, docs[ids.index(c)], q[qi])
+                                            for c in cands[qi]], "full")
+        want = krr.select(full, 3)
+        assert [p.chunk_id for p in res.selected[qi]] == [p.chunk_id for p in want]
+        assert [p.score for p in res.selected[qi]] == [p.score for p in want]
+
+
+def test_sharded_select_on_device_matches_single():
+    """shard.sharded_select host logic with the CUDA top-k kernel, world=1 and
+    a simulated 4-way split merged by the same kernel."""
+    rng = np.random.default_rng(0)
+    n_q, n_c, k = 8, 100, 20
+    cand = np.stack([rng.choice(1000, n_c, replace=False) for _ in range(n_q)])
+    table = np.round(rng.standard_normal((n_q, 1000)), 2).astype(np.float32)
+    want = []
+    for qi in range(n_q):
+        sc = [float(table[qi, d]) for d in cand[qi]]
+        want.append([int(cand[qi][j]) for j in
+                     oracle.select_topk(sc, [f"doc-{d:05d}" for d in cand[qi]], k)])
+    parts = []
+    for r in range(4):
+        w = shard.local_work(cand, r, 4)
+        doc = cand[w.pair_query, w.pair_cand]
+        s = torch.as_tensor(table[w.pair_query, doc], device="cuda")
+        i = torch.as_tensor(doc.astype(np.int32), device="cuda")
+        parts.append(shard.local_topk(s, i, w, n_q, k, engine.segmented_topk))
+    cs = torch.cat([p[0] for p in parts], 1).contiguous()
+    ci = torch.cat([p[1] for p in parts], 1).contiguous()
+    idx, _ = engine.segmented_topk(cs.view(-1), ci.view(-1), n_q, 4 * k, k)
+    got = ci.gather(1, idx.long()).cpu().numpy().tolist()
+    assert got == want

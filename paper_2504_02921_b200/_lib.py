@@ -12,7 +12,8 @@ import os
 
 from .errors import ConfigError, KvRerankError, ShapeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_kvrerank_b200.so")
+LIB_PATH = os.environ.get("KRR_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "_kvrerank_b200.so")
 
 F32, F16, BF16 = 0, 1, 2
 DTYPE_CODES = {"f32": F32, "f16": F16, "bf16": BF16}

@@ -35,7 +35,7 @@ using namespace tc;
 constexpr int TM = 128;        // query rows per CTA = TMEM lanes
 constexpr int STAGES = 2;      // K/V ring depth
 constexpr int THREADS = 192;
-constexpr float RESCALE_LOG2 = 8.0f;   // lazy O rescale threshold (factor 256)
+constexpr float RESCALE_LOG2 = 15.0f;  // lazy O rescale threshold: P <= 2^15 < f16 max
 
 struct Params {
   void* const* prefix_kv;

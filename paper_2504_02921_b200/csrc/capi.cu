@@ -250,7 +250,11 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
     else backend = attention_tcgen05_supported(act, p) ? KRR_ATTN_TCGEN05 : KRR_ATTN_MMA;
   }
   ProfScope ps(s, 1);
-  if (backend == KRR_ATTN_TCGEN05) return launch_attention_tcgen05(act, p, s);
+  if (backend == KRR_ATTN_TCGEN05) {
+    static int v1 = -1;  // KRR_ATTN_TC_V1=1 selects the one-tile-per-CTA kernel (A/B only)
+    if (v1 < 0) { const char* e = getenv("KRR_ATTN_TC_V1"); v1 = (e && atoi(e) == 1) ? 1 : 0; }
+    return v1 ? launch_attention_tcgen05(act, p, s) : launch_attention_pingpong(act, p, s);
+  }
   if (backend == KRR_ATTN_MMA) return launch_attention_mma(act, p, s);
   return launch_attention_simt(act, p, s);
 }

@@ -36,6 +36,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       :: "r"(a), "r"(parity)
       : "memory");
 }
+// Wait without the suspend hint: try_wait still parks the warp for a short
+// hardware-defined window, but the wake-up after the phase flips is faster.
+// Used on latency-critical handoffs (attention softmax <-> MMA).
+__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITF_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITF_%=;\n\t}"
+      :: "r"(a), "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -197,6 +210,18 @@ __device__ __forceinline__ uint64_t sw128_desc_mn(uint32_t saddr, uint32_t lbo_b
   d |= (uint64_t)1u << 46;
   d |= (uint64_t)2u << 61;
   return d;
+}
+// One lane of a converged warp returns true (elect.sync).  Issuing tcgen05.mma
+// from a converged warp under elect lets ptxas keep descriptors in uniform
+// registers (no per-instruction R2UR + elect loop).
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, px;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

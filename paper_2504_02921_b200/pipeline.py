@@ -34,10 +34,19 @@ class RerankResult:
     pairs: int
 
 
+PAD_RANK = np.iinfo(np.int32).max
+
+
 def _id_ranks(chunk_ids_2d) -> np.ndarray:
+    """Rank of every candidate in sorted chunk-id order, [n_q, max_len] int32;
+    ragged rows are padded with PAD_RANK."""
     flat = sorted(set(c for row in chunk_ids_2d for c in row))
     rank = {c: i for i, c in enumerate(flat)}
-    return np.array([[rank[c] for c in row] for row in chunk_ids_2d], dtype=np.int32)
+    n_c = max((len(r) for r in chunk_ids_2d), default=0)
+    out = np.full((len(chunk_ids_2d), n_c), PAD_RANK, dtype=np.int32)
+    for i, row in enumerate(chunk_ids_2d):
+        out[i, :len(row)] = [rank[c] for c in row]
+    return out
 
 
 def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates, keep_m: int,
@@ -45,8 +54,8 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
     """Score every candidate of every query against its cached document KV
     and keep the best ``keep_m`` per query.
 
-    query_tokens: int [n_q, Q] host array; candidates: n_q lists of equal
-    length of chunk ids; doc_tokens: chunk_id -> tokens for miss fallback."""
+    query_tokens: int [n_q, Q] host array; candidates: n_q lists of chunk ids
+    (any lengths); doc_tokens: chunk_id -> tokens for miss fallback."""
     import torch
     if keep_m < 1:
         raise ConfigError("keep_m must be >= 1")
@@ -58,18 +67,20 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
     if any((row != 0).sum() == 0 for row in q):
         from .errors import DegenerateInputError
         raise DegenerateInputError("query is entirely padding")
-    n_c = len(candidates[0]) if n_q else 0
-    if any(len(c) != n_c for c in candidates):
-        raise ShapeError("every query needs the same number of candidates")
+    if len(candidates) != n_q:
+        raise ShapeError("one candidate list per query")
+    lens = np.array([len(c) for c in candidates], dtype=np.int64)
+    n_c = int(lens.max()) if n_q else 0
     flat = [c for row in candidates for c in row]
+    pair_q = np.repeat(np.arange(n_q), lens)
     slots = pool.lookup(flat)
     miss = np.nonzero(slots < 0)[0]
     dev = w.device
-    scores = torch.empty(n_q * n_c, dtype=torch.float32, device=dev)
+    scores = torch.empty(len(flat), dtype=torch.float32, device=dev)
     hit = np.nonzero(slots >= 0)[0]
     q_dev = torch.as_tensor(q.astype(np.int32), device=dev)
     if len(hit):
-        qi = torch.as_tensor(hit // n_c, device=dev)
+        qi = torch.as_tensor(pair_q[hit], device=dev)
         sc = engine.score_slots(w, pool, torch.as_tensor(slots[hit], device=dev),
                                 q_dev.index_select(0, qi))
         scores[torch.as_tensor(hit, device=dev)] = sc
@@ -82,17 +93,25 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
         stage = KVPool(model.config, model.layout.document_len, len(miss), w.dtype, dev)
         st_slots = stage.allocate([f"__miss_{i}" for i in range(len(miss))])
         engine.prefill_slots(w, stage, st_slots, docs, (docs != 0).sum(axis=1))
-        qi = torch.as_tensor(miss // n_c, device=dev)
+        qi = torch.as_tensor(pair_q[miss], device=dev)
         scores[torch.as_tensor(miss, device=dev)] = engine.score_slots(
             w, stage, st_slots, q_dev.index_select(0, qi))
+    if n_c == 0:
+        return RerankResult(list(query_ids), [[] for _ in range(n_q)], 0, 0)
     ids = _id_ranks(candidates)
+    if not (lens == n_c).all():          # ragged: pad segments (-inf sorts last)
+        seg = torch.full((n_q, n_c), float("-inf"), dtype=torch.float32, device=dev)
+        pos = np.arange(len(flat)) - np.repeat(np.cumsum(lens) - lens, lens)
+        seg[torch.as_tensor(pair_q, device=dev), torch.as_tensor(pos, device=dev)] = scores
+        scores = seg.view(-1)
     k = min(keep_m, n_c)
     idx, sc = engine.segmented_topk(scores, ids.reshape(-1), n_q, n_c, k)
     idx_h, sc_h = idx.cpu().numpy(), sc.cpu().numpy()
     selected = [[ScoredPair(chunk_id=candidates[i][int(j)], query_id=query_ids[i],
-                            score=float(s)) for j, s in zip(idx_h[i], sc_h[i]) if j >= 0]
+                            score=float(s)) for j, s in zip(idx_h[i], sc_h[i])
+                 if 0 <= j < lens[i]]
                 for i in range(n_q)]
-    return RerankResult(list(query_ids), selected, int(len(miss)), n_q * n_c)
+    return RerankResult(list(query_ids), selected, int(len(miss)), int(lens.sum()))
 
 
 def populate_store(model: RerankModel, docs, index, store, scheme=None, path: str = "fast",

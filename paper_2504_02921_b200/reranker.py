@@ -223,7 +223,7 @@ def doc_prefill_batch(model: RerankModel, docs_tokens, chunk_ids=None, path: str
     for i in range(n):
         _, valid_lens[i] = _doc_valid(model, docs[i])
     w = model.weights_for(path)
-    pool = pool or pool_for(model, path, n)
+    pool = pool if pool is not None else pool_for(model, path, n)
     anon = [c if c else f"__anon_{id(docs)}_{i}_{np.random.randint(1 << 62)}"
             for i, c in enumerate(chunk_ids)]
     slots = pool.allocate(anon)

@@ -166,7 +166,7 @@ __global__ void score_kernel(const float* __restrict__ x, int T_, int d,
                              const float* __restrict__ head, float* __restrict__ scores) {
   __shared__ float red[32];
   const int b = blockIdx.x;
-  const float* xr = x + ((int64_t)b * T_ + last[b]) * d;
+  const float* xr = x + ((int64_t)b * T_ + (last ? last[b] : 0)) * d;
   float ss = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
   ss = block_sum(ss, red);
@@ -175,6 +175,17 @@ __global__ void score_kernel(const float* __restrict__ x, int T_, int d,
   for (int i = threadIdx.x; i < d; i += blockDim.x) dot = fmaf((xr[i] * inv) * fg[i], head[i], dot);
   dot = block_sum(dot, red);
   if (threadIdx.x == 0) scores[b] = dot;
+}
+
+// Gather the scored row of every sequence: dst[b] = src[b*T + last[b]]
+// (width elements of E bytes), so the last layer's WO/MLP run on n rows only.
+template <typename E>
+__global__ void gather_last_kernel(const E* __restrict__ src, const int32_t* __restrict__ last,
+                                   int T_, int width, E* __restrict__ dst) {
+  const int b = blockIdx.x;
+  const E* s = src + ((int64_t)b * T_ + last[b]) * width;
+  E* o = dst + (int64_t)b * width;
+  for (int i = threadIdx.x; i < width; i += blockDim.x) o[i] = s[i];
 }
 
 // a13: per-segment top-k by (score desc, doc id asc) (pipeline.py:285-287).
@@ -474,6 +485,8 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
   if (rc) return rc;
   const int nqkv = (H + 2 * KVH) * HD;
   const bool prefill_only = b->scores == nullptr;
+  // last-layer row pruning needs the compact buffers to fit the dead regions
+  const bool scoring_tail = !prefill_only && b->last_index != nullptr && b->seq_len >= 4;
   for (int l = 0; l < L; ++l) {
     rc = do_rmsnorm(x, m->attn_gain[l], rows, d, act, xn, s);
     if (rc) return rc;
@@ -496,17 +509,52 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     if (rc) return rc;
     EpiParams er{};
     er.kind = KRR_EPI_RESIDUAL;
+    er.out = x;
+    EpiParams eg{};
+    eg.kind = KRR_EPI_GELU;
+    eg.N = 4 * d;
+    if (scoring_tail && l == L - 1) {
+      // Only the scored row of each sequence reaches the score head
+      // (reranker.py:211-212): run this layer's WO + MLP on n rows.  Compact
+      // buffers reuse regions that are dead by now (q, xn, hb, ab).
+      const int64_t n = b->n_seqs;
+      void* ab_c = qb;                                      // [n, H*HD] act
+      float* x_c = reinterpret_cast<float*>(xn);            // [n, d] f32
+      void* xn_c = hb;                                      // [n, d] act
+      void* hb_c = ab;                                      // [n, 4d] act
+      {
+        ProfScope ps(s, 2);
+        if (es == 2)
+          gather_last_kernel<uint16_t><<<(unsigned)n, 256, 0, s>>>(
+              (const uint16_t*)ab, b->last_index, b->seq_len, H * HD, (uint16_t*)ab_c);
+        else
+          gather_last_kernel<float><<<(unsigned)n, 256, 0, s>>>(
+              (const float*)ab, b->last_index, b->seq_len, H * HD, (float*)ab_c);
+        gather_last_kernel<float><<<(unsigned)n, 256, 0, s>>>(x, b->last_index, b->seq_len, d,
+                                                              x_c);
+        rc = check_launch("gather_last");
+        if (rc) return rc;
+      }
+      er.M = n; er.N = d; er.out = x_c;
+      rc = do_gemm(m->gemm_backend, act, ab_c, m->wo[l], n, d, H * HD, er, s);
+      if (rc) return rc;
+      rc = do_rmsnorm(x_c, m->mlp_gain[l], n, d, act, xn_c, s);
+      if (rc) return rc;
+      eg.M = n; eg.out = hb_c;
+      rc = do_gemm(m->gemm_backend, act, xn_c, m->w_up[l], n, 4 * d, d, eg, s);
+      if (rc) return rc;
+      rc = do_gemm(m->gemm_backend, act, hb_c, m->w_down[l], n, d, 4 * d, er, s);
+      if (rc) return rc;
+      return krr_score_head(x_c, b->n_seqs, 1, d, nullptr, m->final_gain, m->score_head,
+                            b->scores, stream);
+    }
     er.M = rows;
     er.N = d;
-    er.out = x;
     rc = do_gemm(m->gemm_backend, act, ab, m->wo[l], rows, d, H * HD, er, s);
     if (rc) return rc;
     rc = do_rmsnorm(x, m->mlp_gain[l], rows, d, act, xn, s);
     if (rc) return rc;
-    EpiParams eg{};
-    eg.kind = KRR_EPI_GELU;
     eg.M = rows;
-    eg.N = 4 * d;
     eg.out = hb;
     rc = do_gemm(m->gemm_backend, act, xn, m->w_up[l], rows, 4 * d, d, eg, s);
     if (rc) return rc;

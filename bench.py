@@ -35,6 +35,8 @@ CONFIGS = {
     "c1": ("c1_tiny", 64, 1, 64, 20),
     "c2": ("c2_gemma2b", 100, 1, 100, 20),
     "c3": ("c3_mistral7b", 1000, 64, 100, 20),
+    # host-DRAM tier: corpus docs live in pinned host memory, streamed per step
+    "c5": ("c5_mistral7b_d2048", 48, 1, 48, 20),
 }
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x20: "sync_boost", 0x40: "sw_thermal_slowdown",
@@ -203,12 +205,128 @@ def workload_config(args, cfg, lay, corpus, nq, nc, keep):
             "l2": "inputs larger than L2 (KV pool + weights >> 126 MB), no flush"}
 
 
+# ----------------------------------------------------------------- host tier (C5)
+def run_host_tier(args, rank, world, local_rank):
+    """BASELINE config 5: 7B shape, 2048-token docs whose KV lives in pinned
+    host DRAM (the paper's SSD tier stand-in) and is streamed H2D per step,
+    overlapped with scoring (engine.score_host_tier).  Reports pairs/s, the H2D
+    GB/s achieved against the measured pinned-copy peak, and a KV-reuse vs
+    full-recompute sweep over query length."""
+    import torch
+    import paper_2504_02921_b200 as krr
+    from paper_2504_02921_b200 import engine
+    from paper_2504_02921_b200.config import PRESETS
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    preset, corpus, nq, nc, keep = CONFIGS[args.config]
+    corpus = args.corpus or corpus
+    nq = args.queries or nq
+    nc = min(args.cands or nc, corpus)
+    cfg, lay = PRESETS[preset]
+    D = lay.document_len
+    model = krr.RerankModel.build(cfg, lay, precision=args.precision, device=dev)
+    w = model.weights
+    # ---- corpus: prefill in HBM chunks, park every page in the pinned tier
+    chunk = 8
+    tmp = krr.KVPool(cfg, D, chunk, w.dtype, dev)
+    tier = krr.HostKVTier(tmp, corpus)
+    rng = np.random.default_rng(1000 + rank)
+    docs = rng.integers(1, cfg.vocab_size, (corpus, D), dtype=np.int64)
+    for i in range(0, corpus, chunk):
+        j = min(corpus, i + chunk)
+        ids = [f"h{k}" for k in range(i, j)]
+        sl = tmp.allocate(ids)
+        engine.prefill_slots(w, tmp, sl, docs[i:j], np.full(j - i, D))
+        for cid, s in zip(ids, sl):
+            tier.put_from_pool(cid, tmp, int(s))
+            tmp.release(cid)
+    torch.cuda.synchronize()
+    del tmp
+    staging = krr.KVPool(cfg, D, 4, w.dtype, dev)
+    page = tier.slot_bytes
+    # ---- measured H2D peak (pinned -> HBM, 4 pages back to back)
+    cs = torch.cuda.Stream(device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(cs):
+        e0.record(cs)
+        for r in range(3):
+            for k in range(4):
+                staging.slab[k].copy_(tier.slab[k % corpus], non_blocking=True)
+        e1.record(cs)
+    torch.cuda.synchronize()
+    h2d_peak = 12 * page / (e0.elapsed_time(e1) / 1e3) / 1e9
+    crng = np.random.default_rng(100 + rank)
+    qrng = np.random.default_rng(7)
+    sweep = {}
+    qlens = [int(x) for x in args.query_lens.split(",")] if args.query_lens else [lay.query_len]
+    for Q in qlens:
+        q = qrng.integers(1, cfg.vocab_size, (nq, Q), dtype=np.int64)
+        cand = np.stack([crng.choice(corpus, nc, replace=False) for _ in range(nq)])
+        hs = np.asarray(tier.lookup([f"h{c}" for c in cand.reshape(-1)]))
+        qq = np.repeat(q, nc, axis=0)
+
+        def step():
+            sc = engine.score_host_tier(w, tier, staging, hs, qq, copy_stream=cs)
+            return engine.segmented_topk(sc, cand.reshape(-1).astype(np.int32), nq, nc,
+                                         min(keep, nc))
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            step()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / args.steps
+        pairs = nq * nc
+        h2d_bytes = np.unique(hs).size * page
+        # full recompute of the same pairs (prefill D + suffix), sampled on 4 pairs
+        nf = min(4, pairs)
+        st2 = krr.KVPool(cfg, D, nf, w.dtype, dev)
+        sl2 = st2.allocate([f"f{i}" for i in range(nf)])
+
+        def full():
+            engine.prefill_slots(w, st2, sl2, docs[cand.reshape(-1)[:nf]], np.full(nf, D))
+            engine.score_slots(w, st2, sl2, qq[:nf])
+        full()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        full()
+        torch.cuda.synchronize()
+        full_pps = nf / (time.perf_counter() - t0)
+        del st2
+        f_pair = suffix_flops_per_pair(cfg, D, Q)
+        _, peak_s, _, _ = load_peaks()
+        roof = min(peak_s * 1e12 / f_pair, h2d_peak * 1e9 * pairs / h2d_bytes)
+        sweep[Q] = {"pairs_per_s": pairs / (ms / 1e3), "ms_per_step": ms,
+                    "h2d_gbs": h2d_bytes / (ms / 1e3) / 1e9,
+                    "h2d_frac_of_peak": h2d_bytes / (ms / 1e3) / 1e9 / h2d_peak,
+                    "full_recompute_pairs_per_s": full_pps,
+                    "reuse_over_full": pairs / (ms / 1e3) / full_pps,
+                    "pairs_roofline": roof}
+    first = sweep[qlens[0]]
+    out = {"metric": METRIC, "value": first["pairs_per_s"], "unit": "pairs/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": first["ms_per_step"],
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": args.precision, "data": "synthetic",
+           "config": {"workload": f"{preset}: {nq} queries x {nc} docs x {D} tok from a "
+                                  f"{corpus}-doc pinned host tier ({page * corpus / 1e9:.1f} GB), "
+                                  f"streamed H2D per step", "host_docs": corpus,
+                      "page_bytes": page},
+           "h2d_peak_gbs": h2d_peak, "query_len_sweep": sweep}
+    if rank == 0:
+        print(json.dumps(out))
+    return out
+
+
 # ----------------------------------------------------------------- GPU leg
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     import paper_2504_02921_b200 as krr
-    from paper_2504_02921_b200 import _lib, engine, pipeline
+    from paper_2504_02921_b200 import _lib, engine, pipeline, shard
     from paper_2504_02921_b200.config import PRESETS
 
     torch.cuda.set_device(local_rank)
@@ -253,17 +371,10 @@ def run_ours(args, rank, world, local_rank):
     scores = torch.empty(nq * nc, dtype=torch.float32, device=dev)
 
     def merge(idx, sc):
-        """Global top-k: all-gather per-rank (score, doc id), merge on device."""
+        """Global top-k: one all-gather of per-rank (score, doc id), merged on
+        device (paper_2504_02921_b200.shard.merge_topk)."""
         gid = gid_dev.view(nq, nc).gather(1, idx.long())
-        if world == 1:
-            return gid, sc
-        all_sc = [torch.empty_like(sc) for _ in range(world)]
-        all_id = [torch.empty_like(gid) for _ in range(world)]
-        dist.all_gather(all_sc, sc.contiguous())
-        dist.all_gather(all_id, gid.contiguous())
-        cs, ci = torch.cat(all_sc, 1).contiguous(), torch.cat(all_id, 1).contiguous()
-        midx, msc = engine.segmented_topk(cs.view(-1), ci.view(-1), nq, world * k, k)
-        return ci.gather(1, midx.long()), msc
+        return shard.merge_topk(sc, gid, k, engine.segmented_topk)
 
     def step():
         engine.score_slots(w, pool, slots_dev, q_dev.index_select(0, qidx), out=scores)
@@ -308,13 +419,8 @@ def run_ours(args, rank, world, local_rank):
             sc = torch.tensor([[p.score for p in r] for r in res.selected], device=dev)
             gi = torch.tensor([[int(p.chunk_id[4:]) for p in r] for r in res.selected],
                               dtype=torch.int32, device=dev)
-            all_sc = [torch.empty_like(sc) for _ in range(world)]
-            all_id = [torch.empty_like(gi) for _ in range(world)]
-            dist.all_gather(all_sc, sc)
-            dist.all_gather(all_id, gi)
-            cs, ci = torch.cat(all_sc, 1).contiguous(), torch.cat(all_id, 1).contiguous()
-            midx, msc = engine.segmented_topk(cs.view(-1), ci.view(-1), nq, world * k, k)
-            ci.gather(1, midx.long()).cpu()
+            mi, _ = shard.merge_topk(sc, gi, k, engine.segmented_topk)
+            mi.cpu()
         return res
     e2e_step()
     barrier()
@@ -363,11 +469,15 @@ def run_ours(args, rank, world, local_rank):
         gemm_tf = prof["gemm_flops"] / (prof["gemm_ms"] / 1e3) / 1e12 if prof["gemm_ms"] else 0
         f_pair = suffix_flops_per_pair(cfg, D, Q)
         roof_pps = min(peak_s * 1e12 / f_pair, hbm * 1e9 / kv_bytes_per_pair(cfg, D))
-        traffic = None
+        traffic = traffic_alg = None
         tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                tj = json.load(f)
+            traffic, traffic_alg = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
+        # attention kernel: cached-KV bytes it must read per step at HBM bandwidth
+        attn_bytes = nq * nc * kv_bytes_per_pair(cfg, D)
+        attn_gbs = attn_bytes / (prof["attn_ms"] / args.steps / 1e3) / 1e9 if prof["attn_ms"] else 0
         cpu = None
         if not args.no_cpu_baseline:
             v, info = cpu_pairs_per_s(preset, D, Q)
@@ -391,7 +501,13 @@ def run_ours(args, rank, world, local_rank):
                          "gemm_share_of_step": prof["gemm_ms"] / ms if ms else None,
                          "attn_share_of_step": prof["attn_ms"] / ms if ms else None,
                          "misc_share_of_step": prof["misc_ms"] / ms if ms else None,
-                         "pairs_roofline": roof_pps, "pairs_frac": value / world / roof_pps},
+                         "pairs_roofline": roof_pps, "pairs_frac": value / world / roof_pps,
+                         "traffic_launch": "MLP-up GEMM (ncu, profiles/traffic_c3.json)",
+                         "traffic_algorithmic": traffic_alg,
+                         "attention": {"bound": "hbm", "kernel": "attn_pp_kernel (tcgen05)",
+                                       "achieved": attn_gbs, "peak": hbm, "unit": "GB/s",
+                                       "frac": attn_gbs / hbm if hbm else None,
+                                       "bytes_per_step": attn_bytes}},
             "cpu_baseline": cpu,
             "p50_query_latency_ms": float(np.median(lat)) if lat else None,
             "p50_query_latency_candidates": nc,
@@ -418,6 +534,7 @@ def main():
     ap.add_argument("--latency-reps", type=int, default=20)
     ap.add_argument("--full-pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--query-lens", default="", help="C5 sweep, e.g. 16,32,48,64,128,256")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -430,7 +547,10 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
+    if args.config == "c5":
+        run_host_tier(args, rank, world, local_rank)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -244,14 +244,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = cid; tile < tiles; tile += ncl) {
-        int mb, nb;
-        tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cid; tile < tiles; tile += ncl) {
+      int mb, nb;
+      tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one_sync()) {
           // all TMA bytes of the pair land on the leader's barrier
           const uint32_t bar = CG == 2 ? mapa_rank(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
           if (leader) mbar_expect_tx(&full[stage], CG * (C::A_BYTES + C::B_BYTES));
@@ -259,15 +259,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                        mb * C::TILE_M + (int)rank * 128);
           tma_load<CG>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
                        nb * BN + (int)rank * C::B_ROWS);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    // whole warp walks the schedule; one elected lane issues (descriptors stay
+    // in uniform registers, no per-MMA elect loop)
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      const uint64_t dA = sw128_desc(smem_u32(sA));
+      const uint64_t dB = sw128_desc(smem_u32(sB));
       for (int tile = cid; tile < tiles; tile += ncl, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
@@ -277,16 +282,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_f16<CG>(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
-                        (kb | k) != 0);
-          mma_commit<CG>(&empty[stage]);
+            for (int k = 0; k < BK / 16; ++k)
+              mma_f16<CG>(d_tmem, dA + ((stage * C::A_BYTES + k * 32) >> 4),
+                          dB + ((stage * C::B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+            mma_commit<CG>(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit<CG>(&tfull[acc]);
+        if (elect_one_sync()) mma_commit<CG>(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else {

@@ -184,3 +184,56 @@ def segmented_topk(scores, doc_ids, n_seg: int, seg_len: int, k: int):
                                              n_seg, seg_len, k, idx.data_ptr(), sc.data_ptr(),
                                              stream))
     return idx, sc
+
+
+def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_tokens,
+                    copy_stream=None, max_rows: int | None = None):
+    """Score pairs whose document KV lives in the pinned host tier (the paper's
+    SSD/DRAM tier).
+
+    Distinct documents are streamed H2D (cudaMemcpyAsync on ``copy_stream``)
+    into one half of a double-buffered HBM staging pool while the main stream
+    scores every pair of the previously landed half; events order the reuse of
+    each half.  Each document crosses PCIe once per call however many pairs
+    reference it.  Returns f32 [n] scores on the device (pair order)."""
+    import torch
+    if staging.code != w.code:
+        raise ConfigError(f"staging dtype {staging.dtype} != weights dtype {w.dtype}")
+    dev = w.device
+    hs = np.asarray(host_slots, dtype=np.int64)
+    q = torch.as_tensor(np.asarray(q_tokens), device=dev).to(torch.int32)
+    n = hs.size
+    scores = torch.empty(n, dtype=torch.float32, device=dev)
+    if n == 0:
+        return scores
+    half = staging.capacity // 2
+    if half < 1:
+        raise ConfigError("host-tier staging pool needs >= 2 slots")
+    if len(staging):
+        raise ConfigError("host-tier staging pool must be dedicated (empty)")
+    st_slots = np.arange(staging.capacity, dtype=np.int64)
+    docs = np.unique(hs)
+    groups = [docs[i:i + half] for i in range(0, docs.size, half)]
+    main = torch.cuda.current_stream(dev)
+    cs = copy_stream or torch.cuda.Stream(device=dev)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    for gi, grp in enumerate(groups):
+        b = gi & 1
+        slots = st_slots[b * half:b * half + grp.size]
+        with torch.cuda.stream(cs):
+            if gi >= 2:
+                cs.wait_event(free[b])
+            for h, s in zip(grp, slots):
+                staging.slab[int(s)].copy_(tier.slab[int(h)], non_blocking=True)
+            ready[b].record(cs)
+        main.wait_event(ready[b])
+        staging.set_valid_len(slots, tier.valid_len[grp])
+        slot_of = dict(zip(grp.tolist(), slots.tolist()))
+        sel = np.nonzero(np.isin(hs, grp))[0]
+        sel_t = torch.as_tensor(sel, device=dev)
+        sc = score_slots(w, staging, np.array([slot_of[h] for h in hs[sel]]),
+                         q.index_select(0, sel_t), max_rows=max_rows)
+        scores[sel_t] = sc
+        free[b].record(main)
+    return scores

@@ -173,6 +173,12 @@ class HostKVTier:
     def lookup(self, chunk_ids) -> np.ndarray:
         return np.array([self._by_id.get(c, -1) for c in chunk_ids], dtype=np.int64)
 
+    def __len__(self) -> int:
+        return len(self._by_id)
+
+    def __contains__(self, chunk_id: str) -> bool:
+        return chunk_id in self._by_id
+
     def stream_in(self, host_slots, staging: KVPool, staging_slots, stream) -> None:
         """Queue H2D copies of host pages into staging pool slots on ``stream``."""
         import torch

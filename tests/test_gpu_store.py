@@ -166,3 +166,25 @@ def test_sharded_select_on_device_matches_single():
     idx, _ = engine.segmented_topk(cs.view(-1), ci.view(-1), n_q, 4 * k, k)
     got = ci.gather(1, idx.long()).cpu().numpy().tolist()
     assert got == want
+
+
+def test_host_tier_streaming_matches_device_pool(model16):
+    """Docs in the pinned host tier, streamed H2D through a 2x2-slot staging
+    pool on a side stream, score bit-identically to the same docs resident in
+    HBM (batch-invariant kernels; PCIe only moves bytes)."""
+    rng = np.random.default_rng(21)
+    n_docs = 7
+    docs = rng.integers(1, 32768, (n_docs, 128))
+    docs[2, 90:] = 0
+    pool = krr.KVPool(C1[0], 128, n_docs, "f16")
+    slots = pool.allocate([f"d{i}" for i in range(n_docs)])
+    engine.prefill_slots(model16.weights, pool, slots, docs, (docs != 0).sum(axis=1))
+    tier = krr.HostKVTier(pool, n_docs)
+    hslots = [tier.put_from_pool(f"d{i}", pool, int(s)) for i, s in enumerate(slots)]
+    pair_doc = rng.integers(0, n_docs, 20)
+    q = rng.integers(1, 32768, (20, 48))
+    staging = krr.KVPool(C1[0], 128, 4, "f16")
+    got = engine.score_host_tier(model16.weights, tier, staging, np.asarray(hslots)[pair_doc], q)
+    want = engine.score_slots(model16.weights, pool, slots[pair_doc], q)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)

@@ -115,6 +115,12 @@ typedef struct {
   int64_t prefix_pool_bytes;
   const void* cur_pool;
   int64_t cur_pool_bytes;
+  /* layer-split execution (teacher-forced checks, pipelined stacks): when
+   * x_in is set the residual stream starts from it ([n_seqs*seq_len, d] f32)
+   * instead of the embedding; when x_out is set the residual after the last
+   * layer (before the final norm) is copied there and every layer runs in full. */
+  const float* x_in;
+  float* x_out;
 } krr_batch_t;
 
 const char* krr_last_error(void);

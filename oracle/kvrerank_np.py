@@ -211,13 +211,14 @@ def _rotate(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
 
 
 def forward(w: OracleWeights, tokens, positions, past_k=None, past_v=None, valid=None,
-            layer_range=None, x_in=None, capture=None):
+            layer_range=None, x_in=None, capture=None, return_residual=False):
     """Restates ``forward`` (model.py:332-403).
 
     past_k/past_v: [L, KVH, P, HD] f32 (RoPE already applied) or None.
     valid: bool[P+T] or None.  Returns (hidden [T,d] final-normed, new_k, new_v).
     ``layer_range``/``x_in``/``capture`` expose the residual stream for
-    teacher-forced per-layer checks (capture[li] = layer input).
+    teacher-forced per-layer checks (capture[li] = layer input);
+    ``return_residual`` returns the raw residual instead of the final norm.
     """
     cfg = w.cfg
     tokens = np.asarray(tokens, np.int64)
@@ -269,7 +270,7 @@ def forward(w: OracleWeights, tokens, positions, past_k=None, past_v=None, valid
             out[:, kh * G:(kh + 1) * G, :] = o.transpose(1, 0, 2)
         x = x + out.reshape(T, H * HD) @ w.wo[li]                  # model.py:395-397
         x = x + _gelu(_rms(x, w.mlp_gain[li]) @ w.w_up[li]) @ w.w_down[li]  # model.py:399-400
-    return _rms(x, w.final_gain), new_k, new_v
+    return (x if return_residual else _rms(x, w.final_gain)), new_k, new_v
 
 
 # --------------------------------------------------------------------------

@@ -53,7 +53,7 @@ class Batch(C.Structure):
                 ("cur_kv_layers", i32), ("tokens", vp), ("tok_valid", vp), ("prefix_valid_len", vp),
                 ("prefix_kv", vp), ("cur_kv", vp), ("last_index", vp), ("scores", vp),
                 ("prefix_pool", vp), ("prefix_pool_bytes", i64), ("cur_pool", vp),
-                ("cur_pool_bytes", i64)]
+                ("cur_pool_bytes", i64), ("x_in", vp), ("x_out", vp)]
 
 
 _LIB = None

@@ -481,12 +481,20 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
   void* ab = w;                                    w += align256(rows * (int64_t)H * HD * es);
   void* hb = w;
 
-  int rc = krr_embed(b->tokens, m->token_embedding, rows, d, x, stream);
-  if (rc) return rc;
+  int rc = KRR_OK;
+  if (b->x_in) {
+    if (cudaMemcpyAsync(x, b->x_in, rows * d * sizeof(float), cudaMemcpyDeviceToDevice, s) !=
+        cudaSuccess)
+      return fail(KRR_ECUDA, "x_in copy failed");
+  } else {
+    rc = krr_embed(b->tokens, m->token_embedding, rows, d, x, stream);
+    if (rc) return rc;
+  }
   const int nqkv = (H + 2 * KVH) * HD;
-  const bool prefill_only = b->scores == nullptr;
+  const bool prefill_only = b->scores == nullptr && b->x_out == nullptr;
   // last-layer row pruning needs the compact buffers to fit the dead regions
-  const bool scoring_tail = !prefill_only && b->last_index != nullptr && b->seq_len >= 4;
+  const bool scoring_tail = b->scores != nullptr && b->x_out == nullptr &&
+                            b->last_index != nullptr && b->seq_len >= 4;
   for (int l = 0; l < L; ++l) {
     rc = do_rmsnorm(x, m->attn_gain[l], rows, d, act, xn, s);
     if (rc) return rc;
@@ -561,6 +569,10 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     rc = do_gemm(m->gemm_backend, act, hb, m->w_down[l], rows, d, 4 * d, er, s);
     if (rc) return rc;
   }
+  if (b->x_out &&
+      cudaMemcpyAsync(b->x_out, x, rows * d * sizeof(float), cudaMemcpyDeviceToDevice, s) !=
+          cudaSuccess)
+    return fail(KRR_ECUDA, "x_out copy failed");
   if (b->scores) {
     KRR_REQUIRE(b->last_index != nullptr, KRR_ECONFIG, "scores need last_index");
     rc = krr_score_head(x, b->n_seqs, b->seq_len, d, b->last_index, m->final_gain,

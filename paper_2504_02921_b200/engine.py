@@ -64,7 +64,8 @@ def _extent(t):
 
 def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
                 prefix_valid, prefix_ptrs, cur_ptrs, cur_kv_layers: int, last_index=None,
-                scores=None, stream=None, prefix_pool=None, cur_pool=None) -> None:
+                scores=None, stream=None, prefix_pool=None, cur_pool=None, x_in=None,
+                x_out=None) -> None:
     """One krr_forward call over n sequences (all device tensors, contiguous):
     tokens int32 [n, T], tok_valid uint8 [n, T], prefix_valid int32 [n],
     prefix_ptrs / cur_ptrs int64 [n], last_index int32 [n], scores f32 [n].
@@ -81,7 +82,7 @@ def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
     cp, cb = _extent(cur_pool)
     b = _lib.Batch(n, T, pos0, prefix_len, cur_kv_layers, _ptr(tokens), _ptr(tok_valid),
                    _ptr(prefix_valid), _ptr(prefix_ptrs), _ptr(cur_ptrs), _ptr(last_index),
-                   _ptr(scores), pp, pb, cp, cb)
+                   _ptr(scores), pp, pb, cp, cb, _ptr(x_in), _ptr(x_out))
     if stream is None:
         stream = torch.cuda.current_stream(w.device).cuda_stream
     _lib.check(_lib.lib().krr_forward(C.byref(w.struct()), C.byref(b), ws.data_ptr(),
@@ -237,3 +238,56 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
         scores[sel_t] = sc
         free[b].record(main)
     return scores
+
+
+def layer_slice(w: DeviceWeights, l0: int, l1: int):
+    """krr_model_t covering layers [l0, l1) only (layer-split execution with
+    krr_batch_t.x_in / x_out).  KV pointers passed with it must be advanced to
+    layer l0 (``layer_offset_bytes``)."""
+    base = w.struct()
+    cfg = w.config
+    if not (0 <= l0 < l1 <= cfg.layers):
+        raise ConfigError(f"bad layer range [{l0}, {l1})")
+    arr = lambda ts: (C.c_void_p * (l1 - l0))(*[t.data_ptr() for t in ts[l0:l1]])
+    keep = [arr(w.attn_gain), arr(w.mlp_gain), arr(w.wqkv), arr(w.wo), arr(w.w_up),
+            arr(w.w_down)]
+    m = _lib.Model(l1 - l0, cfg.model_dim, cfg.heads, cfg.kv_heads, cfg.head_dim,
+                   cfg.vocab_size, cfg.max_position, w.code, w.gemm_backend, w.attn_backend,
+                   base.token_embedding, base.rope_cos, base.rope_sin, base.final_gain,
+                   base.score_head, *[C.cast(a, C.c_void_p) for a in keep])
+    m._keep = keep
+    return m
+
+
+def layer_offset_bytes(w: DeviceWeights, kv_len: int, layers: int) -> int:
+    """Byte offset of layer ``layers`` inside a [L][2][KVH][kv_len][HD] KV slab."""
+    cfg = w.config
+    es = 4 if w.code == _lib.F32 else 2
+    return layers * 2 * cfg.kv_heads * kv_len * cfg.head_dim * es
+
+
+def run_layers(w: DeviceWeights, l0: int, l1: int, tokens, tok_valid, pos0: int,
+               prefix_len: int, prefix_valid, prefix_ptrs, cur_ptrs, cur_kv_layers: int,
+               x_in=None, x_out=None, prefix_pool=None, cur_pool=None) -> None:
+    """krr_forward over layers [l0, l1) with the residual stream taken from
+    ``x_in`` (or the embedding when None) and written to ``x_out``.  Pointer
+    tables address layer 0 of each slab; they are advanced to l0 here."""
+    import torch
+    n, T = tokens.shape
+    m = layer_slice(w, l0, l1)
+    off_p = layer_offset_bytes(w, prefix_len, l0) if prefix_len else 0
+    off_c = layer_offset_bytes(w, T, l0) if cur_kv_layers > 1 else 0
+    pre = (prefix_ptrs + off_p).contiguous() if prefix_ptrs is not None else None
+    cur = (cur_ptrs + off_c).contiguous()
+    ckl = (l1 - l0) if cur_kv_layers > 1 else 1
+    rows = n * T
+    out = C.c_size_t()
+    _lib.check(_lib.lib().krr_workspace_bytes(C.byref(m), rows, C.byref(out)))
+    ws = _workspace(w.device).get(out.value, w.device)
+    pp, pb = _extent(prefix_pool)
+    cp, cb = _extent(cur_pool)
+    b = _lib.Batch(n, T, pos0, prefix_len, ckl, _ptr(tokens), _ptr(tok_valid),
+                   _ptr(prefix_valid), _ptr(pre), _ptr(cur), 0, 0, pp, pb, cp, cb,
+                   _ptr(x_in), _ptr(x_out))
+    stream = torch.cuda.current_stream(w.device).cuda_stream
+    _lib.check(_lib.lib().krr_forward(C.byref(m), C.byref(b), ws.data_ptr(), ws.numel(), stream))

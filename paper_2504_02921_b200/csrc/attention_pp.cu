@@ -552,7 +552,7 @@ extern "C" int krr_pp_trace_read(unsigned long long* out) {
 #endif
 
 int launch_attention_pingpong(int act_dtype, const AttnParams& p, cudaStream_t s) {
-  if (!attention_tcgen05_supported(act_dtype, p))
+  if (!attention_tcgen05_supported(act_dtype, p) || p.head_dim > 128)
     return fail(KRR_EUNSUPPORTED, "tcgen05 attention needs f16/bf16, head_dim 64|128 and pool bases");
   if (act_dtype == KRR_F16)
     return p.head_dim == 64 ? attn_pp::launch<__half, 64>(p, s) : attn_pp::launch<__half, 128>(p, s);

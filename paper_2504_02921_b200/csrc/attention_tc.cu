@@ -62,7 +62,8 @@ struct Smem {
   static constexpr int P_OFF = V_OFF + STAGES * KV_BYTES;
   static constexpr int BAR_OFF = P_OFF + P_BYTES;
   static constexpr int TOTAL = BAR_OFF + 128;
-  static constexpr int TMEM_COLS = 256;                 // S: 2*KB, O: HD
+  // S: 2*KB, O: HD -> 256 columns (two CTAs per SM) up to HD=128, 512 for HD=256
+  static constexpr int TMEM_COLS = (2 * KB + HD <= 256) ? 256 : 512;
   static_assert(2 * KB + HD <= TMEM_COLS, "TMEM budget");
 };
 
@@ -178,43 +179,50 @@ __global__ void __launch_bounds__(THREADS, 2)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
-      constexpr uint32_t idesc_s = (1u << 4) | (fmt << 7) | (fmt << 10) |
-                                   ((uint32_t)(KB >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
-      constexpr uint32_t idesc_o = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) |
-                                   ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
-      mbar_wait(q_full, 0);
-      for (int j = 0; j <= nb; ++j) {
-        if (j < nb) {
-          const int s = j % STAGES, sb = j & 1;
-          mbar_wait(&k_full[s], (j / STAGES) & 1);
-          mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + s * S::KV_BYTES);
+    // whole warp walks the schedule, one elected lane issues the MMAs
+    constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+    constexpr uint32_t idesc_s = (1u << 4) | (fmt << 7) | (fmt << 10) |
+                                 ((uint32_t)(KB >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+    constexpr uint32_t idesc_o = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) |
+                                 ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+    const uint64_t dQ = sw128_desc(smem_u32(sQ));
+    const uint64_t dK = sw128_desc(smem_u32(sK));
+    const uint64_t dP = sw128_desc(smem_u32(sP));
+    const uint64_t dV = sw128_desc_mn(smem_u32(sV), KB * 128, 1024);
+    mbar_wait(q_full, 0);
+    for (int j = 0; j <= nb; ++j) {
+      if (j < nb) {
+        const int s = j % STAGES, sb = j & 1;
+        mbar_wait(&k_full[s], (j / STAGES) & 1);
+        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one_sync()) {
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k) {
-            const uint32_t off = (k & 3) * 32;
-            mma_f16<1>(tmem + sb * KB, sw128_desc(q0 + (k >> 2) * S::ATOM + off),
-                       sw128_desc(k0 + (k >> 2) * (KB * 128) + off), idesc_s, k > 0);
+            const uint32_t off = (k >> 2) * S::ATOM + (k & 3) * 32;
+            const uint32_t koff = s * S::KV_BYTES + (k >> 2) * (KB * 128) + (k & 3) * 32;
+            mma_f16<1>(tmem + sb * KB, dQ + (off >> 4), dK + (koff >> 4), idesc_s, k > 0);
           }
           mma_commit<1>(&k_empty[s]);
           mma_commit<1>(&s_full[sb]);
         }
-        if (j >= 1) {
-          const int jj = j - 1, s = jj % STAGES;
-          mbar_wait(&v_full[s], (jj / STAGES) & 1);
-          mbar_wait(p_full, jj & 1);
-          tc_fence_after();
-          const uint32_t p0 = smem_u32(sP), v0 = smem_u32(sV + s * S::KV_BYTES);
+        __syncwarp();
+      }
+      if (j >= 1) {
+        const int jj = j - 1, s = jj % STAGES;
+        mbar_wait(&v_full[s], (jj / STAGES) & 1);
+        mbar_wait(p_full, jj & 1);
+        tc_fence_after();
+        if (elect_one_sync()) {
 #pragma unroll
           for (int k = 0; k < KB / 16; ++k)
-            mma_f16<1>(tmem + O_COL, sw128_desc(p0 + (k >> 2) * S::ATOM + (k & 3) * 32),
-                       sw128_desc_mn(v0 + k * 16 * 128, KB * 128, 1024), idesc_o,
+            mma_f16<1>(tmem + O_COL, dP + (((k >> 2) * S::ATOM + (k & 3) * 32) >> 4),
+                       dV + ((s * S::KV_BYTES + k * 16 * 128) >> 4), idesc_o,
                        (jj > 0) || (k > 0));
           mma_commit<1>(&v_empty[s]);
           mma_commit<1>(pv_done);
         }
+        __syncwarp();
       }
     }
   } else {
@@ -438,7 +446,8 @@ static int launch(const AttnParams& a, cudaStream_t s) {
 }
 
 bool supported(int act, const AttnParams& a) {
-  return (act == KRR_F16 || act == KRR_BF16) && (a.head_dim == 64 || a.head_dim == 128) &&
+  return (act == KRR_F16 || act == KRR_BF16) &&
+         (a.head_dim == 64 || a.head_dim == 128 || a.head_dim == 256) &&
          a.cur_pool != nullptr && a.cur_pool_bytes > 0 &&
          (a.prefix_len == 0 || (a.prefix_pool != nullptr && a.prefix_pool_bytes > 0));
 }
@@ -447,13 +456,16 @@ bool supported(int act, const AttnParams& a) {
 
 int launch_attention_tcgen05(int act_dtype, const AttnParams& p, cudaStream_t s) {
   if (!attn_tc::supported(act_dtype, p))
-    return fail(KRR_EUNSUPPORTED, "tcgen05 attention needs f16/bf16, head_dim 64|128 and pool bases");
+    return fail(KRR_EUNSUPPORTED, "tcgen05 attention needs f16/bf16, head_dim 64|128|256 and pool bases");
   constexpr int KB = 64;
-  if (act_dtype == KRR_F16)
-    return p.head_dim == 64 ? attn_tc::launch<__half, 64, KB>(p, s)
-                            : attn_tc::launch<__half, 128, KB>(p, s);
-  return p.head_dim == 64 ? attn_tc::launch<__nv_bfloat16, 64, KB>(p, s)
-                          : attn_tc::launch<__nv_bfloat16, 128, KB>(p, s);
+  if (act_dtype == KRR_F16) {
+    if (p.head_dim == 64) return attn_tc::launch<__half, 64, KB>(p, s);
+    if (p.head_dim == 128) return attn_tc::launch<__half, 128, KB>(p, s);
+    return attn_tc::launch<__half, 256, KB>(p, s);
+  }
+  if (p.head_dim == 64) return attn_tc::launch<__nv_bfloat16, 64, KB>(p, s);
+  if (p.head_dim == 128) return attn_tc::launch<__nv_bfloat16, 128, KB>(p, s);
+  return attn_tc::launch<__nv_bfloat16, 256, KB>(p, s);
 }
 
 bool attention_tcgen05_supported(int act_dtype, const AttnParams& p) {
@@ -474,6 +486,7 @@ static int occupancy(int* out) {
 
 int attention_tcgen05_occupancy(int act_dtype, int head_dim, int* out) {
   KRR_REQUIRE(head_dim == 64 || head_dim == 128, KRR_EUNSUPPORTED, "head_dim 64|128");
+  // (head_dim 256 runs one CTA per SM by design: 512 TMEM columns)
   if (act_dtype == KRR_BF16)
     return head_dim == 64 ? occupancy<__nv_bfloat16, 64>(out) : occupancy<__nv_bfloat16, 128>(out);
   return head_dim == 64 ? occupancy<__half, 64>(out) : occupancy<__half, 128>(out);

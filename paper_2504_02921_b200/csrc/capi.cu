@@ -264,7 +264,10 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
   if (backend == KRR_ATTN_TCGEN05) {
     static int v1 = -1;  // KRR_ATTN_TC_V1=1 selects the one-tile-per-CTA kernel (A/B only)
     if (v1 < 0) { const char* e = getenv("KRR_ATTN_TC_V1"); v1 = (e && atoi(e) == 1) ? 1 : 0; }
-    return v1 ? launch_attention_tcgen05(act, p, s) : launch_attention_pingpong(act, p, s);
+    // ping-pong kernel for head_dim 64/128; the one-tile kernel covers 256 (its
+    // O accumulator needs 256 TMEM columns, so two tiles cannot share an SM)
+    return (v1 || p.head_dim == 256) ? launch_attention_tcgen05(act, p, s)
+                                     : launch_attention_pingpong(act, p, s);
   }
   if (backend == KRR_ATTN_MMA) return launch_attention_mma(act, p, s);
   return launch_attention_simt(act, p, s);

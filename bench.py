@@ -35,6 +35,9 @@ CONFIGS = {
     "c1": ("c1_tiny", 64, 1, 64, 20),
     "c2": ("c2_gemma2b", 100, 1, 100, 20),
     "c3": ("c3_mistral7b", 1000, 64, 100, 20),
+    # C4 per-GPU shard: 2,500 chunks x 67 MB = 168 GB of KV resident in one GPU's HBM
+    # (x8 GPUs = the 20k-chunk corpus); top-20 merged across ranks
+    "c4": ("c3_mistral7b", 2500, 64, 100, 20),
     # host-DRAM tier: corpus docs live in pinned host memory, streamed per step
     "c5": ("c5_mistral7b_d2048", 48, 1, 48, 20),
 }
@@ -230,7 +233,7 @@ def run_host_tier(args, rank, world, local_rank):
     # ---- corpus: prefill in HBM chunks, park every page in the pinned tier
     chunk = 8
     tmp = krr.KVPool(cfg, D, chunk, w.dtype, dev)
-    tier = krr.HostKVTier(tmp, corpus)
+    tier = krr.HostKVTier(tmp, corpus, quant=args.host_quant or None)
     rng = np.random.default_rng(1000 + rank)
     docs = rng.integers(1, cfg.vocab_size, (corpus, D), dtype=np.int64)
     for i in range(0, corpus, chunk):
@@ -248,14 +251,16 @@ def run_host_tier(args, rank, world, local_rank):
     # ---- measured H2D peak (pinned -> HBM, 4 pages back to back)
     cs = torch.cuda.Stream(device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    probe = torch.empty(staging.slab[0].numel(), dtype=staging.slab.dtype, pin_memory=True)
     with torch.cuda.stream(cs):
         e0.record(cs)
         for r in range(3):
             for k in range(4):
-                staging.slab[k].copy_(tier.slab[k % corpus], non_blocking=True)
+                staging.slab[k].view(-1).copy_(probe, non_blocking=True)
         e1.record(cs)
     torch.cuda.synchronize()
-    h2d_peak = 12 * page / (e0.elapsed_time(e1) / 1e3) / 1e9
+    h2d_peak = 12 * staging.slot_bytes / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del probe
     crng = np.random.default_rng(100 + rank)
     qrng = np.random.default_rng(7)
     sweep = {}
@@ -312,9 +317,10 @@ def run_host_tier(args, rank, world, local_rank):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": args.precision, "data": "synthetic",
            "config": {"workload": f"{preset}: {nq} queries x {nc} docs x {D} tok from a "
-                                  f"{corpus}-doc pinned host tier ({page * corpus / 1e9:.1f} GB), "
-                                  f"streamed H2D per step", "host_docs": corpus,
-                      "page_bytes": page},
+                                  f"{corpus}-doc pinned host tier ({page * corpus / 1e9:.1f} GB, "
+                                  f"{args.host_quant or 'f16'}), streamed H2D per step",
+                      "host_docs": corpus, "page_bytes_over_pcie": page,
+                      "host_quant": args.host_quant or None},
            "h2d_peak_gbs": h2d_peak, "query_len_sweep": sweep}
     if rank == 0:
         print(json.dumps(out))
@@ -449,7 +455,7 @@ def run_ours(args, rank, world, local_rank):
             if i >= 2:
                 lat.append((time.perf_counter() - t0) * 1e3)
         # ---- same-box full-recompute GPU baseline (prefill + suffix, same kernels)
-        nf = min(args.full_pairs, corpus)
+        nf = min(args.full_pairs, corpus, 8 if args.config == "c4" else corpus)
         st = krr.KVPool(cfg, D, nf, w.dtype, dev)
         st_slots = st.allocate([f"f{i}" for i in range(nf)])
 
@@ -514,6 +520,10 @@ def run_ours(args, rank, world, local_rank):
             "full_recompute_pairs_per_s": full_pps,
             "reuse_over_full": value / world / full_pps,
             "prefill_docs_per_s": corpus / prefill_s,
+            "hbm": {"kv_pool_gb": pool.slab.numel() * pool.slab.element_size() / 1e9,
+                    "weights_gb": w.nbytes() / 1e9,
+                    "max_allocated_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+                    "device_total_gb": torch.cuda.get_device_properties(dev).total_memory / 1e9},
             "model_build_s": t_build,
         }
         print(json.dumps(out))
@@ -535,6 +545,8 @@ def main():
     ap.add_argument("--full-pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--query-lens", default="", help="C5 sweep, e.g. 16,32,48,64,128,256")
+    ap.add_argument("--host-quant", default="", choices=["", "int8", "int4"],
+                    help="C5: keep host-tier pages HRKV-quantised (2x/4x fewer PCIe bytes)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -23,6 +23,8 @@
  *   krr_score_head        <- model.py:402 final norm + reranker.py:211-212 last-row dot
  *   krr_segmented_topk    <- pipeline.py:285-287 _select
  *   krr_dequant_kv        <- codec.py:82-95 dequantize_tensor (INT8/INT4 -> 16-bit pool page)
+ *   krr_quant_pages       <- codec.py:58-79 quantize_tensor, batched over a page's 2L tensors
+ *   krr_dequant_pages     <- codec.py:82-95 dequantize_tensor, batched (host-tier INT8/INT4)
  */
 #ifndef KVRERANK_B200_H
 #define KVRERANK_B200_H
@@ -170,6 +172,16 @@ int krr_segmented_topk(const float* scores, const int32_t* doc_ids, int32_t n_se
 int krr_dequant_kv(const uint8_t* codes, const float* scales, int32_t bits, int32_t kv_heads,
                    int32_t doc_len, int32_t head_dim, int out_dtype, void* out,
                    krr_stream_t stream);
+
+/* Batched HRKV quantisation of n tensors [KVH][D][HD] (e.g. one pool page = 2L
+ * tensors): scales [n][KVH][HD] f32; codes per tensor KVH*D*HD bytes (INT8) or
+ * (KVH*D*HD+1)/2 bytes (INT4, low nibble first).  Bit-identical to the host codec. */
+int krr_quant_pages(const void* src, int src_dtype, int32_t n_tensors, int32_t kv_heads,
+                    int32_t doc_len, int32_t head_dim, int32_t bits, uint8_t* codes,
+                    float* scales, krr_stream_t stream);
+int krr_dequant_pages(const uint8_t* codes, const float* scales, int32_t bits, int32_t n_tensors,
+                      int32_t kv_heads, int32_t doc_len, int32_t head_dim, int out_dtype,
+                      void* out, krr_stream_t stream);
 
 #ifdef __cplusplus
 }

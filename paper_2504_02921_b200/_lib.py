@@ -27,6 +27,7 @@ EXPORTS = (
     "krr_last_error", "krr_version", "krr_launch_count", "krr_workspace_bytes", "krr_forward",
     "krr_profile_enable", "krr_profile_read", "krr_init_uniform", "krr_embed", "krr_rmsnorm",
     "krr_gemm", "krr_attention", "krr_attention_occupancy", "krr_score_head", "krr_segmented_topk", "krr_dequant_kv",
+    "krr_quant_pages", "krr_dequant_pages",
 )
 
 vp = C.c_void_p
@@ -86,6 +87,8 @@ def lib():
         L.krr_score_head.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp]
         L.krr_segmented_topk.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
         L.krr_dequant_kv.argtypes = [vp, vp, i32, i32, i32, i32, C.c_int, vp, vp]
+        L.krr_quant_pages.argtypes = [vp, C.c_int, i32, i32, i32, i32, i32, vp, vp, vp]
+        L.krr_dequant_pages.argtypes = [vp, vp, i32, i32, i32, i32, i32, C.c_int, vp, vp]
         _LIB = L
     return _LIB
 

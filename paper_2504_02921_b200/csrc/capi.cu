@@ -241,6 +241,73 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ codes, const float* _
   }
 }
 
+// codec.py:58-79 quantize_tensor, batched over n tensors [KVH][D][HD] (a whole
+// pool page is 2L tensors).  Block = (tensor, kv head); thread i owns channels
+// 2i, 2i+1.  scale = amax/level (1.0 for an all-zero channel), code =
+// clamp(sign(y)*floor(|y|+0.5), +-level) with y = x/scale -- the reference's
+// f32 operation order, so codes are bit-identical to the host codec.
+// INT4 packs channel pairs low nibble first; each tensor is packed separately
+// ((KVH*D*HD+1)/2 bytes), as in the HRKV payload.
+template <typename T>
+__global__ void quant_pages_kernel(const T* __restrict__ src, int D, int HD, int KVH, int bits,
+                                   uint8_t* __restrict__ codes, float* __restrict__ scales) {
+  const int t = blockIdx.x / KVH, h = blockIdx.x - t * KVH;
+  const int c = 2 * threadIdx.x;
+  if (c >= HD) return;
+  const int64_t tensor_elems = (int64_t)KVH * D * HD;
+  const T* x = src + t * tensor_elems + (int64_t)h * D * HD;
+  float a0 = 0.f, a1 = 0.f;
+  for (int d = 0; d < D; ++d) {
+    a0 = fmaxf(a0, fabsf(Act<T>::to(x[(int64_t)d * HD + c])));
+    a1 = fmaxf(a1, fabsf(Act<T>::to(x[(int64_t)d * HD + c + 1])));
+  }
+  const float level = bits == 8 ? 127.f : 7.f;
+  const float s0 = a0 == 0.f ? 1.f : __fdiv_rn(a0, level);
+  const float s1 = a1 == 0.f ? 1.f : __fdiv_rn(a1, level);
+  float* so = scales + ((int64_t)t * KVH + h) * HD;
+  so[c] = s0;
+  so[c + 1] = s1;
+  const int64_t tensor_bytes = bits == 8 ? tensor_elems : (tensor_elems + 1) / 2;
+  uint8_t* co = codes + t * tensor_bytes;
+  for (int d = 0; d < D; ++d) {
+    const int64_t e = ((int64_t)h * D + d) * HD + c;
+    const float y0 = __fdiv_rn(Act<T>::to(x[(int64_t)d * HD + c]), s0);
+    const float y1 = __fdiv_rn(Act<T>::to(x[(int64_t)d * HD + c + 1]), s1);
+    const float r0 = fminf(fmaxf(copysignf(floorf(__fadd_rn(fabsf(y0), 0.5f)), y0), -level), level);
+    const float r1 = fminf(fmaxf(copysignf(floorf(__fadd_rn(fabsf(y1), 0.5f)), y1), -level), level);
+    const int q0 = (int)r0, q1 = (int)r1;
+    if (bits == 8) {
+      co[e] = (uint8_t)(int8_t)q0;
+      co[e + 1] = (uint8_t)(int8_t)q1;
+    } else {
+      co[e >> 1] = (uint8_t)((q0 & 0xF) | ((q1 & 0xF) << 4));   // e even: low nibble first
+    }
+  }
+}
+
+// codec.py:82-95 dequantize_tensor, batched over n tensors (whole page).
+template <typename T>
+__global__ void dequant_pages_kernel(const uint8_t* __restrict__ codes,
+                                     const float* __restrict__ scales, int n, int bits, int KVH,
+                                     int D, int HD, T* __restrict__ out) {
+  const int64_t te = (int64_t)KVH * D * HD;
+  const int64_t tb = bits == 8 ? te : (te + 1) / 2;
+  const int64_t total = te * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / te, r = i - t * te;
+    int code;
+    if (bits == 8) code = (int)(int8_t)codes[t * tb + r];
+    else {
+      const uint8_t byte = codes[t * tb + (r >> 1)];
+      code = (((r & 1) ? (byte >> 4) : (byte & 0xF)) ^ 8) - 8;
+    }
+    const int h = (int)(r / ((int64_t)D * HD));
+    const int c = (int)(r % HD);
+    out[i] = Act<T>::from((float)code * scales[(t * KVH + h) * HD + c]);
+  }
+}
+
 static unsigned grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   const int64_t cap = (int64_t)device_sm_count() * 32;
@@ -442,6 +509,46 @@ int krr_dequant_kv(const uint8_t* codes, const float* scales, int32_t bits, int3
     dequant_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(codes, scales, bits, kv_heads, doc_len, head_dim,
                                                     (__nv_bfloat16*)out);
   return check_launch("dequant_kv");
+}
+
+int krr_quant_pages(const void* src, int src_dtype, int32_t n_tensors, int32_t kv_heads,
+                    int32_t doc_len, int32_t head_dim, int32_t bits, uint8_t* codes,
+                    float* scales, krr_stream_t stream) {
+  KRR_REQUIRE(bits == 8 || bits == 4, KRR_ECONFIG, "quant bits must be 8 or 4");
+  KRR_REQUIRE(head_dim % 2 == 0 && head_dim <= 2048, KRR_ESHAPE, "head_dim must be even");
+  if (n_tensors == 0) return KRR_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned blocks = (unsigned)(n_tensors * kv_heads), threads = (unsigned)(head_dim / 2);
+  if (src_dtype == KRR_F32)
+    quant_pages_kernel<float><<<blocks, threads, 0, s>>>((const float*)src, doc_len, head_dim,
+                                                          kv_heads, bits, codes, scales);
+  else if (src_dtype == KRR_F16)
+    quant_pages_kernel<__half><<<blocks, threads, 0, s>>>((const __half*)src, doc_len, head_dim,
+                                                           kv_heads, bits, codes, scales);
+  else
+    quant_pages_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(
+        (const __nv_bfloat16*)src, doc_len, head_dim, kv_heads, bits, codes, scales);
+  return check_launch("quant_pages");
+}
+
+int krr_dequant_pages(const uint8_t* codes, const float* scales, int32_t bits, int32_t n_tensors,
+                      int32_t kv_heads, int32_t doc_len, int32_t head_dim, int out_dtype,
+                      void* out, krr_stream_t stream) {
+  KRR_REQUIRE(bits == 8 || bits == 4, KRR_ECONFIG, "dequant bits must be 8 or 4");
+  if (n_tensors == 0) return KRR_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned g = grid_for((int64_t)n_tensors * kv_heads * doc_len * head_dim, 256);
+  if (out_dtype == KRR_F32)
+    dequant_pages_kernel<float><<<g, 256, 0, s>>>(codes, scales, n_tensors, bits, kv_heads,
+                                                  doc_len, head_dim, (float*)out);
+  else if (out_dtype == KRR_F16)
+    dequant_pages_kernel<__half><<<g, 256, 0, s>>>(codes, scales, n_tensors, bits, kv_heads,
+                                                   doc_len, head_dim, (__half*)out);
+  else
+    dequant_pages_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(codes, scales, n_tensors, bits,
+                                                          kv_heads, doc_len, head_dim,
+                                                          (__nv_bfloat16*)out);
+  return check_launch("dequant_pages");
 }
 
 // ------------------------------------------------------------- layer loop

@@ -46,7 +46,17 @@ def workspace_bytes(w: DeviceWeights, rows: int) -> int:
     return out.value
 
 
-def rows_budget(w: DeviceWeights, budget: int = DEFAULT_WORKSPACE_BUDGET) -> int:
+def rows_budget(w: DeviceWeights, budget: int | None = None) -> int:
+    """Rows per krr_forward call: at most DEFAULT_WORKSPACE_BUDGET of
+    activations, and no more than ~80% of what is free on the device (plus the
+    workspace already held), so a pool that fills most of the 180 GB HBM
+    (C4: 2,500 x 67 MB pages per GPU) still runs in smaller chunks."""
+    import torch
+    if budget is None:
+        free, _ = torch.cuda.mem_get_info(w.device)
+        held = _workspace(w.device).buf
+        held = held.numel() if held is not None else 0
+        budget = min(DEFAULT_WORKSPACE_BUDGET, int(0.8 * (free + held)))
     per_row = workspace_bytes(w, 1 << 16) / float(1 << 16)
     return max(1, int(budget // per_row))
 
@@ -226,7 +236,7 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
             if gi >= 2:
                 cs.wait_event(free[b])
             for h, s in zip(grp, slots):
-                staging.slab[int(s)].copy_(tier.slab[int(h)], non_blocking=True)
+                tier.copy_in(int(h), staging, int(s), int(s))
             ready[b].record(cs)
         main.wait_event(ready[b])
         staging.set_valid_len(slots, tier.valid_len[grp])

@@ -146,18 +146,59 @@ class KVPool:
 
 class HostKVTier:
     """Pinned host-DRAM tier with the pool's slot layout, streamed into an HBM
-    staging pool on a side stream (cudaMemcpyAsync via torch copy_)."""
+    staging pool on a side stream (cudaMemcpyAsync via torch copy_).
 
-    def __init__(self, pool_like: KVPool, capacity: int):
+    ``quant="int8"|"int4"`` stores pages in the HRKV quantised form instead
+    (codec.py:58-115: per-(kv_head, channel) scales, one tensor per (layer,
+    K|V)): the GPU quantises on put (krr_quant_pages, bit-identical to the
+    host codec), 2x / 4x fewer bytes cross PCIe, and the staging copy is
+    expanded back to 16-bit by krr_dequant_pages on the copy stream."""
+
+    BITS = {None: 16, "int8": 8, "int4": 4}
+
+    def __init__(self, pool_like: KVPool, capacity: int, quant: str | None = None):
         import torch
+        if quant not in self.BITS:
+            raise StoreError(f"unknown host-tier quantisation {quant!r}")
         self.page_shape = pool_like.page_shape
         self.dtype = pool_like.slab.dtype
+        self.code = pool_like.code
         self.capacity = capacity
-        self.slab = torch.empty((capacity, *self.page_shape), dtype=self.dtype, pin_memory=True)
-        self.slot_bytes = pool_like.slot_bytes
+        self.quant = quant
+        L, _, KVH, D, HD = self.page_shape
+        self.n_tensors, self.tensor_elems = 2 * L, KVH * D * HD
+        if quant is None:
+            self.slab = torch.empty((capacity, *self.page_shape), dtype=self.dtype,
+                                    pin_memory=True)
+            self.slot_bytes = pool_like.slot_bytes
+        else:
+            bits = self.BITS[quant]
+            tb = self.tensor_elems if bits == 8 else (self.tensor_elems + 1) // 2
+            self.code_bytes = self.n_tensors * tb
+            self.scale_elems = self.n_tensors * KVH * HD
+            self.codes = torch.empty((capacity, self.code_bytes), dtype=torch.uint8,
+                                     pin_memory=True)
+            self.scales = torch.empty((capacity, self.scale_elems), dtype=torch.float32,
+                                      pin_memory=True)
+            self.slot_bytes = self.code_bytes + 4 * self.scale_elems   # bytes over PCIe
         self.valid_len = np.zeros(capacity, dtype=np.int64)
         self._by_id: dict[str, int] = {}
         self._next = 0
+        self._dev = {}
+
+    @property
+    def bits(self) -> int:
+        return self.BITS[self.quant]
+
+    def _device_bufs(self, device, n: int):
+        """Device landing buffers for n quantised pages (codes, scales)."""
+        import torch
+        key = (str(device), n)
+        if key not in self._dev:
+            self._dev = {key: (torch.empty((n, self.code_bytes), dtype=torch.uint8, device=device),
+                               torch.empty((n, self.scale_elems), dtype=torch.float32,
+                                           device=device))}
+        return self._dev[key]
 
     def put_from_pool(self, chunk_id: str, pool: KVPool, slot: int) -> int:
         if chunk_id not in self._by_id:
@@ -166,9 +207,37 @@ class HostKVTier:
             self._by_id[chunk_id] = self._next
             self._next += 1
         h = self._by_id[chunk_id]
-        self.slab[h].copy_(pool.slab[slot])
+        if self.quant is None:
+            self.slab[h].copy_(pool.slab[slot])
+        else:
+            import torch
+            codes, scales = self._device_bufs(pool.device, 1)
+            L_, KVH, D, HD = self.page_shape[0], *self.page_shape[2:]
+            stream = torch.cuda.current_stream(pool.device).cuda_stream
+            _lib.check(_lib.lib().krr_quant_pages(
+                pool.slab[slot].data_ptr(), pool.code, self.n_tensors, KVH, D, HD, self.bits,
+                codes.data_ptr(), scales.data_ptr(), stream))
+            self.codes[h].copy_(codes[0])
+            self.scales[h].copy_(scales[0])
         self.valid_len[h] = pool.host_valid_len(slot)
         return h
+
+    def copy_in(self, h: int, staging: KVPool, s: int, k: int = 0) -> None:
+        """Queue the H2D transfer of host page h into staging slot s on the
+        current stream (plus the dequant kernel for a quantised tier; k picks
+        the device landing buffer)."""
+        import torch
+        if self.quant is None:
+            staging.slab[s].copy_(self.slab[h], non_blocking=True)
+            return
+        codes, scales = self._device_bufs(staging.device, staging.capacity)
+        codes[k].copy_(self.codes[h], non_blocking=True)
+        scales[k].copy_(self.scales[h], non_blocking=True)
+        KVH, D, HD = self.page_shape[2:]
+        stream = torch.cuda.current_stream(staging.device).cuda_stream
+        _lib.check(_lib.lib().krr_dequant_pages(
+            codes[k].data_ptr(), scales[k].data_ptr(), self.bits, self.n_tensors, KVH, D, HD,
+            staging.code, staging.slab[s].data_ptr(), stream))
 
     def lookup(self, chunk_ids) -> np.ndarray:
         return np.array([self._by_id.get(c, -1) for c in chunk_ids], dtype=np.int64)
@@ -184,5 +253,5 @@ class HostKVTier:
         import torch
         with torch.cuda.stream(stream):
             for h, s in zip(host_slots, staging_slots):
-                staging.slab[int(s)].copy_(self.slab[int(h)], non_blocking=True)
+                self.copy_in(int(h), staging, int(s), int(s))
         staging.set_valid_len(staging_slots, self.valid_len[np.asarray(host_slots)])

@@ -1,0 +1,19 @@
+#!/bin/bash
+# Round evidence: GPU tests, smoke, C3 bench (default line), launch list + ncu full captures
+# of the GEMM and the attention kernel, C4 capacity run.
+TAG=${1:-r01z}
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+timeout -s KILL 1200 python -m pytest tests -q -m gpu --timeout 900 -p no:cacheprovider -s > gpurun_out/${TAG}_pytest.log 2>&1
+echo "pytest rc=$?"; grep -E "passed|failed|^FAILED|layer" gpurun_out/${TAG}_pytest.log | tail -12
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/${TAG}_smoke.log
+timeout -s KILL 1200 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+echo "bench rc=$?"; python scripts/show.py gpurun_out/${TAG}_bench.json
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --latency-reps 0 --full-pairs 4"
+timeout -s KILL 1200 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_launches.log 2>&1
+echo "ncu list rc=$?"
+timeout -s KILL 1200 ncu --nvtx --nvtx-include "timed/" --set full --clock-control none --import-source on -k regex:"gemm_tcgen05" -s 2 -c 1 -o gpurun_out/${TAG}_gemm_full $CMD > gpurun_out/${TAG}_gemm_full.log 2>&1
+echo "ncu gemm rc=$?"
+timeout -s KILL 900 ncu --nvtx --nvtx-include "timed/" --set full --clock-control none --import-source on -k regex:"attn_pp" -c 1 -o gpurun_out/${TAG}_attn_full $CMD > gpurun_out/${TAG}_attn_full.log 2>&1
+echo "ncu attn rc=$?"
+timeout -s KILL 1500 python bench.py --config c4 --steps 3 --warmup 2 --latency-reps 5 --no-cpu-baseline > gpurun_out/${TAG}_c4.json 2> gpurun_out/${TAG}_c4.err
+echo "c4 rc=$?"; python scripts/show.py gpurun_out/${TAG}_c4.json; tail -2 gpurun_out/${TAG}_c4.err

@@ -188,3 +188,67 @@ def test_host_tier_streaming_matches_device_pool(model16):
     want = engine.score_slots(model16.weights, pool, slots[pair_doc], q)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("bits,scheme", [(8, codec.QuantScheme.INT8_PER_CHANNEL),
+                                         (4, codec.QuantScheme.INT4_PER_CHANNEL)])
+@pytest.mark.parametrize("src", ["f32", "f16"])
+def test_quant_pages_bit_exact_vs_host_codec(bits, scheme, src):
+    """krr_quant_pages / krr_dequant_pages == codec.quantize_tensor /
+    dequantize_tensor (the reference's codec.py:58-95 semantics), tensor by tensor."""
+    from paper_2504_02921_b200 import _lib
+    rng = np.random.default_rng(bits)
+    n, KVH, D, HD = 4, 2, 37, 64                       # odd D*... exercises int4 packing
+    x = (rng.standard_normal((n, KVH, D, HD)) * 3).astype(np.float32)
+    x[1, 0, :, 5] = 0.0                                 # all-zero channel -> scale 1
+    x[2, 1, 3, 7] = 2.5                                 # exact .5 tie after scaling is likely
+    if src == "f16":
+        x = x.astype(np.float16).astype(np.float32)
+    xt = torch.as_tensor(x, device="cuda").to(torch.float16 if src == "f16" else torch.float32)
+    te = KVH * D * HD
+    tb = te if bits == 8 else (te + 1) // 2
+    codes = torch.empty(n * tb, dtype=torch.uint8, device="cuda")
+    scales = torch.empty(n * KVH * HD, dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().krr_quant_pages(xt.data_ptr(), _lib.F16 if src == "f16" else _lib.F32,
+                                          n, KVH, D, HD, bits, codes.data_ptr(),
+                                          scales.data_ptr(), s))
+    out = torch.empty(n, KVH, D, HD, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().krr_dequant_pages(codes.data_ptr(), scales.data_ptr(), bits, n, KVH, D,
+                                            HD, _lib.F32, out.data_ptr(), s))
+    torch.cuda.synchronize()
+    c_h, s_h, o_h = codes.cpu().numpy(), scales.cpu().numpy(), out.cpu().numpy()
+    for t in range(n):
+        q, sc = codec.quantize_tensor(x[t], scheme)
+        assert c_h[t * tb:(t + 1) * tb].tobytes() == q, t
+        assert np.array_equal(s_h[t * KVH * HD:(t + 1) * KVH * HD].reshape(KVH, HD), sc), t
+        assert np.array_equal(o_h[t], codec.dequantize_tensor(q, sc, scheme, (KVH, D, HD))), t
+
+
+@pytest.mark.parametrize("quant,scheme", [("int8", codec.QuantScheme.INT8_PER_CHANNEL),
+                                          ("int4", codec.QuantScheme.INT4_PER_CHANNEL)])
+def test_quantised_host_tier_matches_hrkv_entries(model16, quant, scheme):
+    """A quantised host tier scores exactly like the same docs stored as HRKV
+    INT8/INT4 entries (reference codec) and decoded into HBM."""
+    rng = np.random.default_rng(31)
+    n_docs = 5
+    docs = rng.integers(1, 32768, (n_docs, 128))
+    pool = krr.KVPool(C1[0], 128, n_docs, "f16")
+    slots = pool.allocate([f"d{i}" for i in range(n_docs)])
+    engine.prefill_slots(model16.weights, pool, slots, docs, np.full(n_docs, 128))
+    tier = krr.HostKVTier(pool, n_docs, quant=quant)
+    hs = np.array([tier.put_from_pool(f"d{i}", pool, int(s)) for i, s in enumerate(slots)])
+    assert tier.slot_bytes < pool.slot_bytes
+    ref_pool = krr.KVPool(C1[0], 128, n_docs, "f16")
+    ref_slots = []
+    for i, s in enumerate(slots):
+        kv = krr.DocKV(f"e{i}", krr.DeviceKV(pool, int(s)), 128)
+        entry = codec.encode_entry(kv, scheme)
+        ref_slots.append(codec.decode_entry_to_pool(entry, ref_pool).kv.slot)
+    pair_doc = rng.integers(0, n_docs, 12)
+    q = rng.integers(1, 32768, (12, 48))
+    staging = krr.KVPool(C1[0], 128, 2, "f16")
+    got = engine.score_host_tier(model16.weights, tier, staging, hs[pair_doc], q)
+    want = engine.score_slots(model16.weights, ref_pool, np.array(ref_slots)[pair_doc], q)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)

@@ -1,0 +1,547 @@
+// Persistent ping-pong tensor-core attention with P kept in TMEM (sm_100a).
+//
+// Same semantics as attention.cu (model.py:349-394, _exp_rows :406-436).
+// Relative to attention_pp.cu this kernel removes the shared-memory traffic
+// that bounded it (MMA operand reads of P, the softmax's P stores):
+//
+//  * P (16-bit) is written by the softmax warps straight back into the TMEM
+//    columns that held S (tcgen05.st) and consumed as the TMEM A operand of
+//    O += P.V (tcgen05.mma ... [a_tmem]) -- no smem round trip;
+//  * per tile two S/P buffers of 64 keys and one O (2 tiles x (2*64 + HD)
+//    columns = 512 for HD=128).  S runs two blocks ahead of the softmax: the
+//    issue order  PV_X(j), S_X(j+2)  relies on the tensor pipe executing
+//    tcgen05.mma in order, so S_X(j+2) overwrites P_X(j) (same buffer) only
+//    after PV_X(j) has read it;
+//  * the rare lazy O rescale waits for the previous P.V (per-buffer barrier);
+//  * the suffix-block mask (tok_valid, causal) comes from a 64-bit ballot mask,
+//    not per-key global loads.
+//
+// Work item = (unit, pair of 128-row tiles) as in attention_pp.cu.
+// SMEM: Q_A|Q_B 64 KB, K ring 4 x 16 KB, V ring 4 x 16 KB = 192 KB.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <math_constants.h>
+#include <mutex>
+#include "launchers.h"
+#include "tc_ptx.cuh"
+
+namespace krr {
+namespace attn_fa {
+using namespace tc;
+#define mbar_wait mbar_wait_fast   // latency-critical handoffs: no suspend hint
+#ifdef KRR_PP_TRACE
+__device__ unsigned long long g_fa_trace[16 * 8 * 64];
+#define TR(role, ev, gidx)                                                        \
+  do {                                                                            \
+    if (blockIdx.x == 0 && (gidx) < 64 && (threadIdx.x & 31) == 0)                \
+      g_fa_trace[((role) * 8 + (ev)) * 64 + (gidx)] = clock64();                  \
+  } while (0)
+#else
+#define TR(role, ev, gidx) do {} while (0)
+#endif
+
+constexpr int TM = 128;
+constexpr int KB = 64;
+constexpr int NK = 4, NV = 4;   // K / V ring depth
+constexpr int THREADS = 320;    // w0 producers (lanes 0 Q, 1 K, 2 V), w1 MMA, w2-5 / w6-9 softmax
+constexpr float RESCALE_LOG2 = 15.0f;   // P <= 2^15 < f16 max
+
+struct Params {
+  void* const* prefix_kv;
+  const char* prefix_base;
+  int64_t prefix_page_bytes;
+  void* const* cur_kv;
+  const char* cur_base;
+  int64_t cur_page_bytes;
+  const int32_t* prefix_valid_len;
+  const uint8_t* tok_valid;
+  void* out;
+  int KVH, G, T, P, layer, cur_layer, R, pairs, items;
+};
+
+template <int HD>
+struct Smem {
+  static constexpr int ATOM_Q = TM * 128;                // one 128-row swizzle column of Q
+  static constexpr int ATOM_KV = KB * 128;               // one 128-key swizzle column of K/V
+  static constexpr int Q_TILE = (HD / 64) * ATOM_Q;
+  static constexpr int KV_BYTES = (HD / 64) * ATOM_KV;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + 2 * Q_TILE;
+  static constexpr int V_OFF = K_OFF + NK * KV_BYTES;
+  static constexpr int BAR_OFF = V_OFF + NV * KV_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 512;
+  static_assert(2 * KB + HD <= 256, "TMEM budget per tile");
+};
+
+enum {
+  B_QFULL = 0, B_QEMPTY, B_KFULL, B_KEMPTY = B_KFULL + NK, B_VFULL = B_KEMPTY + NK,
+  B_VEMPTY = B_VFULL + NV, B_SFULL = B_VEMPTY + NV /*[tile][buf]*/, B_PFULL = B_SFULL + 4,
+  B_PVDONE = B_PFULL + 4 /*[tile][buf]*/, B_ODONE = B_PVDONE + 4, B_OEMPTY = B_ODONE + 2,
+  B_COUNT = B_OEMPTY + 2
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t pack_2(float a, float b) {
+  if constexpr (std::is_same<T, __half>::value) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
+// O += P.V with P (A operand) in TMEM, V (B operand) from smem.
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+struct Item {
+  int unit, b, kvh, row0, nb_pre, nb, vlen, t_max;
+};
+__device__ __forceinline__ Item item_of(const Params& p, int it) {
+  Item x;
+  x.unit = it / p.pairs;
+  const int pair = it - x.unit * p.pairs;
+  x.b = x.unit / p.KVH;
+  x.kvh = x.unit - x.b * p.KVH;
+  x.row0 = pair * 2 * TM;
+  const int last_row = min(x.row0 + 2 * TM, p.R) - 1;
+  x.t_max = (last_row / p.T != x.row0 / p.T) ? p.T - 1 : last_row % p.T;
+  x.vlen = p.P ? min(p.prefix_valid_len[x.b], p.P) : 0;
+  x.nb_pre = (x.vlen + KB - 1) / KB;
+  x.nb = x.nb_pre + (x.t_max + 1 + KB - 1) / KB;
+  return x;
+}
+
+template <typename T, int HD>
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_fa_kernel(const __grid_constant__ CUtensorMap tmQ,
+                   const __grid_constant__ CUtensorMap tmPre,
+                   const __grid_constant__ CUtensorMap tmCur, const Params p) {
+  using S = Smem<HD>;
+  extern __shared__ uint8_t smem[];
+  uint8_t* sQ = smem + S::Q_OFF;
+  uint8_t* sK = smem + S::K_OFF;
+  uint8_t* sV = smem + S::V_OFF;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    if ((smem_u32(smem) & 1023) != 0) __trap();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmPre)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur)) : "memory");
+    mbar_init(&bar[B_QFULL], 1);
+    mbar_init(&bar[B_QEMPTY], 1);
+    for (int s = 0; s < NK; ++s) { mbar_init(&bar[B_KFULL + s], 1); mbar_init(&bar[B_KEMPTY + s], 1); }
+    for (int s = 0; s < NV; ++s) { mbar_init(&bar[B_VFULL + s], 1); mbar_init(&bar[B_VEMPTY + s], 1); }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&bar[B_SFULL + i], 1);
+      mbar_init(&bar[B_PFULL + i], 4);
+      mbar_init(&bar[B_PVDONE + i], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&bar[B_ODONE + x], 1);
+      mbar_init(&bar[B_OEMPTY + x], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producers
+    if (lane == 0) {                                   // Q tiles, per item
+      int n = 0;
+      for (int it = blockIdx.x; it < p.items; it += gridDim.x, ++n) {
+        const Item x = item_of(p, it);
+        mbar_wait(&bar[B_QEMPTY], (n & 1) ^ 1);
+        mbar_expect_tx(&bar[B_QFULL], 2 * S::Q_TILE);
+#pragma unroll
+        for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load<1>(sQ + tile * S::Q_TILE + a * S::ATOM_Q, &tmQ, smem_u32(&bar[B_QFULL]),
+                        a * 64, x.unit * p.R + x.row0 + tile * TM);
+      }
+    } else if (lane < 3) {                             // K ring (lane 1), V ring (lane 2)
+      const bool is_k = lane == 1;
+      const int nst = is_k ? NK : NV;
+      uint64_t* full = &bar[is_k ? B_KFULL : B_VFULL];
+      uint64_t* empty = &bar[is_k ? B_KEMPTY : B_VEMPTY];
+      uint8_t* ring = is_k ? sK : sV;
+      int g = 0;
+      for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+        const Item x = item_of(p, it);
+        const int pre_page = p.P ? (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b]) -
+                                          p.prefix_base) / p.prefix_page_bytes) +
+                                       (p.layer * 2) * p.KVH + x.kvh
+                                 : 0;
+        const int cur_page = (int)((reinterpret_cast<const char*>(p.cur_kv[x.b]) - p.cur_base) /
+                                   p.cur_page_bytes) + (p.cur_layer * 2) * p.KVH + x.kvh;
+        const int vofs = is_k ? 0 : p.KVH;
+        for (int j = 0; j < x.nb; ++j, ++g) {
+          const int s = g % nst;
+          mbar_wait(&empty[s], ((g / nst) & 1) ^ 1);
+          mbar_expect_tx(&full[s], S::KV_BYTES);
+          const bool pre = j < x.nb_pre;
+          const CUtensorMap* map = pre ? &tmPre : &tmCur;
+          const int key0 = (pre ? j : j - x.nb_pre) * KB;
+          const int pk = (pre ? pre_page : cur_page) + vofs;
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load3(ring + s * S::KV_BYTES + a * S::ATOM_KV, map, &full[s], a * 64, key0, pk);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+    constexpr uint32_t idesc_s = (1u << 4) | (fmt << 7) | (fmt << 10) |
+                                 ((uint32_t)(KB >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+    constexpr uint32_t idesc_o = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) |
+                                 ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+    const uint64_t dQ = sw128_desc(smem_u32(sQ));
+    const uint64_t dK = sw128_desc(smem_u32(sK));
+    const uint64_t dV = sw128_desc_mn(smem_u32(sV), S::ATOM_KV, 1024);
+    int g = 0, n = 0;
+    // S_tile(gs) = Q_tile . K(gs)^T into S buffer gs&1
+    auto issue_s = [&](int tile, int gs) {
+      const int st = gs % NK;
+      if (elect_one_sync()) {
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t qoff = tile * S::Q_TILE + (k >> 2) * S::ATOM_Q + (k & 3) * 32;
+          const uint32_t koff = st * S::KV_BYTES + (k >> 2) * S::ATOM_KV + (k & 3) * 32;
+          mma_f16<1>(tmem + tile * 256 + (gs & 1) * KB, dQ + (qoff >> 4), dK + (koff >> 4),
+                     idesc_s, k > 0);
+        }
+        mma_commit<1>(&bar[B_SFULL + tile * 2 + (gs & 1)]);
+      }
+      __syncwarp();
+    };
+    // O_tile += P_tile(gs) . V(gs), P in the first KB/2 columns of S buffer gs&1
+    auto issue_pv = [&](int tile, int gs, bool acc) {
+      const int sv = gs % NV;
+      if (elect_one_sync()) {
+#pragma unroll
+        for (int k = 0; k < KB / 16; ++k)
+          mma_ts(tmem + tile * 256 + 2 * KB, tmem + tile * 256 + (gs & 1) * KB + k * 8,
+                 dV + ((sv * S::KV_BYTES + k * 16 * 128) >> 4), idesc_o, acc || k > 0);
+        mma_commit<1>(&bar[B_PVDONE + tile * 2 + (gs & 1)]);
+      }
+      __syncwarp();
+    };
+    auto issue_s_pair = [&](int gs, bool last_s) {     // S(gs) for both tiles, release K
+      mbar_wait(&bar[B_KFULL + gs % NK], (gs / NK) & 1);
+      tc_fence_after();
+      issue_s(0, gs);
+      issue_s(1, gs);
+      if (elect_one_sync()) {
+        mma_commit<1>(&bar[B_KEMPTY + gs % NK]);
+        if (last_s) mma_commit<1>(&bar[B_QEMPTY]);      // Q no longer read by this item
+      }
+      __syncwarp();
+    };
+    for (int it = blockIdx.x; it < p.items; it += gridDim.x, ++n) {
+      const Item x = item_of(p, it);
+      mbar_wait(&bar[B_QFULL], n & 1);
+      issue_s_pair(g, x.nb == 1);
+      if (x.nb > 1) issue_s_pair(g + 1, x.nb == 2);
+      for (int j = 0; j < x.nb; ++j) {
+        const int gs = g + j;
+        const bool ahead = j + 2 < x.nb;
+        mbar_wait(&bar[B_VFULL + gs % NV], (gs / NV) & 1);
+        if (ahead) mbar_wait(&bar[B_KFULL + (gs + 2) % NK], ((gs + 2) / NK) & 1);
+#pragma unroll
+        for (int tile = 0; tile < 2; ++tile) {
+          if (j == 0) mbar_wait(&bar[B_OEMPTY + tile], (n & 1) ^ 1);
+          mbar_wait(&bar[B_PFULL + tile * 2 + (gs & 1)], (gs >> 1) & 1);
+          TR(2, tile * 2, gs);
+          tc_fence_after();
+          issue_pv(tile, gs, j > 0);
+          if (ahead) issue_s(tile, gs + 2);   // in-order pipe: PV(gs) reads P before S(gs+2) lands
+          else if (j == x.nb - 1 && elect_one_sync()) mma_commit<1>(&bar[B_ODONE + tile]);
+          __syncwarp();
+          TR(2, tile * 2 + 1, gs);
+        }
+        if (elect_one_sync()) {
+          mma_commit<1>(&bar[B_VEMPTY + gs % NV]);
+          if (ahead) {
+            mma_commit<1>(&bar[B_KEMPTY + (gs + 2) % NK]);
+            if (j + 2 == x.nb - 1) mma_commit<1>(&bar[B_QEMPTY]);
+          }
+        }
+        __syncwarp();
+      }
+      g += x.nb;
+    }
+  } else {
+    // ---------------------------------------------------------- softmax WGs
+    const int tile = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int lrow = quad * 32 + lane;
+    const uint32_t lane_base = tmem + tile * 256 + ((uint32_t)(quad * 32) << 16);
+    const uint32_t o_col = 2 * KB;
+    uint64_t* s_full = &bar[B_SFULL + tile * 2];    // [buf]
+    uint64_t* p_full = &bar[B_PFULL + tile * 2];    // [buf]
+    uint64_t* pv_done = &bar[B_PVDONE + tile * 2];  // [buf]
+    const float L2E = 1.4426950408889634f;
+    const int T_ = p.T;
+    const int H = p.KVH * p.G;
+    int g = 0, n = 0;
+    for (int it = blockIdx.x; it < p.items; it += gridDim.x, ++n) {
+      const Item x = item_of(p, it);
+      const int r = x.row0 + tile * TM + lrow;
+      const bool row_ok = r < p.R;
+      const bool quad_live = x.row0 + tile * TM + quad * 32 < p.R;
+      const int gq = r / T_, t = r - gq * T_;
+      const uint8_t* tv = p.tok_valid + (int64_t)x.b * T_;
+      float m_use = -CUDART_INF_F, l = 0.f;
+      for (int j = 0; j < x.nb; ++j) {
+        const int gs = g + j, sb = gs & 1;
+        const bool pre = j < x.nb_pre;
+        const int key0 = (pre ? j : j - x.nb_pre) * KB;
+        // suffix block: visible keys as a 64-bit mask (tok_valid ballot, then causal)
+        uint64_t cur_mask = ~0ull;
+        if (!pre) {
+          const int k_lo = key0 + lane, k_hi = key0 + 32 + lane;
+          const uint32_t lo = __ballot_sync(0xffffffffu, k_lo < T_ && __ldg(tv + k_lo));
+          const uint32_t hi = __ballot_sync(0xffffffffu, k_hi < T_ && __ldg(tv + k_hi));
+          cur_mask = ((uint64_t)hi << 32) | lo;
+          const int rel = t - key0;                     // keys key0+c visible iff c <= rel
+          cur_mask &= rel >= 63 ? ~0ull : (rel < 0 ? 0ull : ((2ull << rel) - 1));
+        }
+        mbar_wait(&s_full[sb], (gs >> 1) & 1);
+        if (quad == 2) TR(3 + tile, 0, gs);
+        tc_fence_after();
+        bool need = false;
+        float alpha = 1.f;
+        float sv[KB];
+        if (quad_live) {
+          {
+            uint32_t raw[KB / 32][32];
+#pragma unroll
+            for (int c = 0; c < KB / 32; ++c)
+              tmem_ld32_nowait(lane_base + sb * KB + c * 32, raw[c]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < KB / 32; ++c)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(raw[c][i]);
+          }
+          if (quad == 2) TR(3 + tile, 1, gs);
+          if (!pre) {
+#pragma unroll
+            for (int c = 0; c < KB; ++c)
+              if (!((cur_mask >> c) & 1ull)) sv[c] = -CUDART_INF_F;
+          } else if (key0 + KB > x.vlen) {
+#pragma unroll
+            for (int c = 0; c < KB; ++c)
+              if (key0 + c >= x.vlen) sv[c] = -CUDART_INF_F;
+          }
+          float m8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) m8[e] = fmaxf(sv[e], sv[e + 8]);
+#pragma unroll
+          for (int c = 16; c < KB; c += 8)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], sv[c + e]);
+          float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                           fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+          mx = row_ok ? mx * L2E : -CUDART_INF_F;
+          need = mx > m_use + RESCALE_LOG2;
+          if (need) {
+            alpha = ex2_approx(m_use - mx);
+            m_use = mx;
+          }
+        }
+        if (quad_live && j >= 1 && __any_sync(0xffffffffu, need)) {
+          // O must be stable: wait for P.V of block gs-1 (its buffer's barrier)
+          mbar_wait(&pv_done[(gs - 1) & 1], ((gs - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32_nowait(lane_base + o_col + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(lane_base + o_col + c * 32, o);
+          }
+        }
+        if (quad == 2) TR(3 + tile, 2, gs);
+        if (quad_live) {
+          const float neg_m = !row_ok ? -CUDART_INF_F : (m_use == -CUDART_INF_F) ? 0.f : -m_use;
+          float l4[4] = {0.f, 0.f, 0.f, 0.f};
+          uint32_t w[KB / 2];
+#pragma unroll
+          for (int i = 0; i < KB / 2; ++i) {
+            const float p0 = ex2_approx(fmaf(sv[2 * i], L2E, neg_m));
+            const float p1 = ex2_approx(fmaf(sv[2 * i + 1], L2E, neg_m));
+            l4[i & 3] += p0 + p1;
+            w[i] = pack_2<T>(p0, p1);
+          }
+          tmem_st32(lane_base + sb * KB, w);          // P over the S columns it came from
+          l = l * alpha + ((l4[0] + l4[1]) + (l4[2] + l4[3]));
+        }
+        tmem_st_wait();
+        if (quad == 2) TR(3 + tile, 3, gs);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+      }
+      // ---------------------------------------------------------- epilogue
+      mbar_wait(&bar[B_ODONE + tile], n & 1);
+      tc_fence_after();
+      if (quad_live) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        T* dst = reinterpret_cast<T*>(p.out) + ((int64_t)x.b * T_ + t) * (H * HD) +
+                 (int64_t)(x.kvh * p.G + gq) * HD;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32_nowait(lane_base + o_col + c * 32, o);
+          tmem_ld_wait();
+          if (row_ok) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                w[e] = pack_2<T>(__uint_as_float(o[q4 * 8 + 2 * e]) * inv,
+                                 __uint_as_float(o[q4 * 8 + 2 * e + 1]) * inv);
+              d4[q4] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar[B_OEMPTY + tile]);
+      g += x.nb;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+static int encode(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int rank,
+                  const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
+  auto enc = encoder();
+  if (!enc) return fail(KRR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, dt, rank, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(KRR_ECUDA, "attention tensor map encode failed: " + std::to_string((int)r));
+  return KRR_OK;
+}
+
+template <typename T, int HD>
+static int launch(const AttnParams& a, cudaStream_t s) {
+  using Sm = Smem<HD>;
+  const CUtensorMapDataType dt = std::is_same<T, __half>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                                : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const int R = a.group * a.seq_len;
+  const int64_t units = (int64_t)a.n_seqs * a.kv_heads;
+  const int pairs = (R + 2 * TM - 1) / (2 * TM);
+  KRR_REQUIRE(units * R < INT32_MAX && units * pairs < INT32_MAX, KRR_ESHAPE,
+              "attention batch too large");
+  CUtensorMap mq, mp, mc;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)(units * R)};
+    cuuint64_t str[1] = {(cuuint64_t)HD * sizeof(T)};
+    cuuint32_t box[2] = {64, TM};
+    int rc = encode(&mq, a.q, dt, 2, dims, str, box);
+    if (rc) return rc;
+  }
+  const int64_t cur_page = (int64_t)a.seq_len * HD * sizeof(T);
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)HD, (cuuint64_t)a.seq_len,
+                          (cuuint64_t)(a.cur_pool_bytes / cur_page)};
+    cuuint64_t str[2] = {(cuuint64_t)HD * sizeof(T), (cuuint64_t)cur_page};
+    cuuint32_t box[3] = {64, (cuuint32_t)KB, 1};
+    int rc = encode(&mc, a.cur_pool, dt, 3, dims, str, box);
+    if (rc) return rc;
+  }
+  const int64_t pre_page = (int64_t)std::max(a.prefix_len, 1) * HD * sizeof(T);
+  if (a.prefix_len > 0) {
+    cuuint64_t dims[3] = {(cuuint64_t)HD, (cuuint64_t)a.prefix_len,
+                          (cuuint64_t)(a.prefix_pool_bytes / pre_page)};
+    cuuint64_t str[2] = {(cuuint64_t)HD * sizeof(T), (cuuint64_t)pre_page};
+    cuuint32_t box[3] = {64, (cuuint32_t)KB, 1};
+    int rc = encode(&mp, a.prefix_pool, dt, 3, dims, str, box);
+    if (rc) return rc;
+  } else {
+    mp = mc;
+  }
+  const int items = (int)(units * pairs);
+  Params p{a.prefix_kv, static_cast<const char*>(a.prefix_pool), pre_page, a.cur_kv,
+           static_cast<const char*>(a.cur_pool), cur_page, a.prefix_valid_len, a.tok_valid,
+           a.out, a.kv_heads, a.group, a.seq_len, a.prefix_len, a.layer, a.cur_layer, R,
+           pairs, items};
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_fa_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Sm::TOTAL);
+    attr = true;
+  }
+  const int grid = std::min(items, device_sm_count());
+  attn_fa_kernel<T, HD><<<grid, THREADS, Sm::TOTAL, s>>>(mq, mp, mc, p);
+  return check_launch("attention_fa");
+}
+
+}  // namespace attn_fa
+
+#ifdef KRR_PP_TRACE
+extern "C" int krr_fa_trace_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, attn_fa::g_fa_trace, sizeof(attn_fa::g_fa_trace)) == cudaSuccess ? 0 : 3;
+}
+#endif
+
+int launch_attention_fa(int act_dtype, const AttnParams& p, cudaStream_t s) {
+  if (!attention_tcgen05_supported(act_dtype, p) || p.head_dim > 128)
+    return fail(KRR_EUNSUPPORTED, "TMEM-P attention needs f16/bf16, head_dim 64|128 and pool bases");
+  if (act_dtype == KRR_F16)
+    return p.head_dim == 64 ? attn_fa::launch<__half, 64>(p, s) : attn_fa::launch<__half, 128>(p, s);
+  return p.head_dim == 64 ? attn_fa::launch<__nv_bfloat16, 64>(p, s)
+                          : attn_fa::launch<__nv_bfloat16, 128>(p, s);
+}
+
+}  // namespace krr

@@ -1,6 +1,7 @@
 // C ABI entry points (include/kvrerank_b200.h), small kernels, and the
 // layer-loop driver krr_forward.
 #include <math_constants.h>
+#include <cstring>
 #include <mutex>
 #include <vector>
 #include "launchers.h"
@@ -329,12 +330,17 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
   }
   ProfScope ps(s, 1);
   if (backend == KRR_ATTN_TCGEN05) {
-    static int v1 = -1;  // KRR_ATTN_TC_V1=1 selects the one-tile-per-CTA kernel (A/B only)
-    if (v1 < 0) { const char* e = getenv("KRR_ATTN_TC_V1"); v1 = (e && atoi(e) == 1) ? 1 : 0; }
-    // ping-pong kernel for head_dim 64/128; the one-tile kernel covers 256 (its
-    // O accumulator needs 256 TMEM columns, so two tiles cannot share an SM)
-    return (v1 || p.head_dim == 256) ? launch_attention_tcgen05(act, p, s)
-                                     : launch_attention_pingpong(act, p, s);
+    // KRR_ATTN_TC_KERNEL = fa (default: P in TMEM) | pp (P via smem) | v1 (one tile/CTA);
+    // A/B switch, fixed per process.  head_dim 256 always uses the one-tile
+    // kernel (its O accumulator needs 256 TMEM columns).
+    static int which = -1;
+    if (which < 0) {
+      const char* e = getenv("KRR_ATTN_TC_KERNEL");
+      which = !e ? 0 : (!strcmp(e, "pp") ? 1 : !strcmp(e, "v1") ? 2 : 0);
+    }
+    if (which == 2 || p.head_dim == 256) return launch_attention_tcgen05(act, p, s);
+    if (which == 1) return launch_attention_pingpong(act, p, s);
+    return launch_attention_fa(act, p, s);
   }
   if (backend == KRR_ATTN_MMA) return launch_attention_mma(act, p, s);
   return launch_attention_simt(act, p, s);

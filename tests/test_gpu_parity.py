@@ -191,3 +191,26 @@ def test_wide_shapes_f32(golden_dir, name):
 def test_wide_shapes_f16(golden_dir, name):
     s, r = _wide(golden_dir, name, "f16")
     assert normwise(s, r) <= F16_NORMWISE, normwise(s, r)
+
+
+def test_yes_no_head_is_two_row_logit_difference(c1_golden):
+    """head='yes_no': score == logit(yes) - logit(no) of a tied lm_head on the
+    last valid token, computed from the final-normed hidden state that the
+    default head dots with score_head (self-consistency; outside reference parity)."""
+    m = krr.RerankModel.build(*C1, precision="f32", head="yes_no", yes_no_ids=(11, 7))
+    docs, q = c1_golden["doc_tokens"][:3], c1_golden["query_tokens"]
+    kvs = krr.doc_prefill_batch(m, docs, [f"yn{i}" for i in range(3)])
+    res, _ = krr.score_batch(m, [("q", k.chunk_id, k, q) for k in kvs], "reuse")
+    import oracle
+    ow = oracle.init_weights(oracle.OracleConfig(layers=2, model_dim=256, heads=4, kv_heads=2,
+                                                 head_dim=64, vocab_size=32768,
+                                                 document_len=128, query_len=48))
+    emb = m.weights.token_embedding.cpu().numpy()
+    v = emb[11] - emb[7]
+    for r, d in zip(res, docs):
+        kk, vv, vl = oracle.doc_prefill(ow, d)
+        D = kk.shape[2]
+        hidden, _, _ = oracle.forward(ow, q, np.arange(D, D + q.size), kk, vv,
+                                      np.concatenate([np.arange(D) < vl, q != 0]))
+        want = float(hidden[int(np.nonzero(q != 0)[0][-1])] @ v)
+        assert abs(r.score - want) <= 1e-4 * max(1.0, abs(want))

@@ -246,7 +246,7 @@ def run_host_tier(args, rank, world, local_rank):
             tmp.release(cid)
     torch.cuda.synchronize()
     del tmp
-    staging = krr.KVPool(cfg, D, 4, w.dtype, dev)
+    staging = krr.KVPool(cfg, D, args.staging_slots, w.dtype, dev)
     page = tier.slot_bytes
     # ---- measured H2D peak (pinned -> HBM, 4 pages back to back)
     cs = torch.cuda.Stream(device=dev)
@@ -510,7 +510,7 @@ def run_ours(args, rank, world, local_rank):
                          "pairs_roofline": roof_pps, "pairs_frac": value / world / roof_pps,
                          "traffic_launch": "MLP-up GEMM (ncu, profiles/traffic_c3.json)",
                          "traffic_algorithmic": traffic_alg,
-                         "attention": {"bound": "hbm", "kernel": "attn_pp_kernel (tcgen05)",
+                         "attention": {"bound": "hbm", "kernel": "attn_fa_kernel (tcgen05, P in TMEM)",
                                        "achieved": attn_gbs, "peak": hbm, "unit": "GB/s",
                                        "frac": attn_gbs / hbm if hbm else None,
                                        "bytes_per_step": attn_bytes}},
@@ -545,6 +545,8 @@ def main():
     ap.add_argument("--full-pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--query-lens", default="", help="C5 sweep, e.g. 16,32,48,64,128,256")
+    ap.add_argument("--staging-slots", type=int, default=16,
+                    help="C5: HBM staging slots (two halves, double-buffered)")
     ap.add_argument("--host-quant", default="", choices=["", "int8", "int4"],
                     help="C5: keep host-tier pages HRKV-quantised (2x/4x fewer PCIe bytes)")
     args = ap.parse_args()

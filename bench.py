@@ -553,6 +553,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run every rank on one device (e.g. a 2-rank gloo check of the
+    # N>1 code path on a single-GPU box); never used for reported numbers
+    if os.environ.get("KRR_BENCH_ONE_DEVICE"):
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -560,7 +564,11 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("KRR_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     if args.config == "c5":
         run_host_tier(args, rank, world, local_rank)
     else:

@@ -307,7 +307,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
+      // one epilogue warp polls the accumulator barrier; the other three are
+      // parked on a named barrier (the poll loop of four warps was ~1/4 of all
+      // issued instructions and power)
+      if (warp == 2) mbar_wait(&tfull[acc], acc_phase);
+      named_bar_sync(1, 128);
       tc_fence_after();
       const int64_t row0 = (int64_t)mb * C::TILE_M + rank * 128 + quad * 32;
 #pragma unroll 1
@@ -424,11 +428,17 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (ep.kind == KRR_EPI_QKV_ROPE && ep.qkv.head_dim % 32 != 0)
     return launch_gemm_simt(act_dtype, A, B, M, N, K, ep, s);  // a chunk must stay in one head
 
-  static int mode = -1;  // KRR_GEMM_CTA=1|2 picks the tile shape (default 1); fixed per process
-  if (mode < 0) {
+  // Tile shape: KRR_GEMM_CTA=1 (128x256 per CTA) | 2 (256x256 per CTA pair,
+  // cta_group::2) | 3 = per-shape choice (2 for K <= 4096, 1 for the deep-K
+  // down projection).  Read once per process; default 1 (measured best overall
+  // on the power-capped C3 step).
+  static int env_mode = -1;
+  if (env_mode < 0) {
     const char* e = getenv("KRR_GEMM_CTA");
-    mode = (e && atoi(e) == 2) ? 2 : 1;
+    env_mode = e ? atoi(e) : 1;
+    if (env_mode < 1 || env_mode > 3) env_mode = 1;
   }
+  const int mode = env_mode == 3 ? (K <= 4096 && M >= 1024 ? 2 : 1) : env_mode;
   const CUtensorMapDataType dt =
       act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const int tile_m = mode == 2 ? 256 : 128;

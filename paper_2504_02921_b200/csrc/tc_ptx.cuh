@@ -223,6 +223,11 @@ __device__ __forceinline__ bool elect_one_sync() {
       : "=r"(pred));
   return pred != 0;
 }
+// Named CTA barrier over `count` threads: waiting warps are parked by the
+// hardware (no issue slots, unlike an mbarrier try_wait poll loop).
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

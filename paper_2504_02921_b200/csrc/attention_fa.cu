@@ -266,8 +266,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int j = 0; j < x.nb; ++j) {
         const int gs = g + j;
         const bool ahead = j + 2 < x.nb;
+        TR(2, 4, gs);
         mbar_wait(&bar[B_VFULL + gs % NV], (gs / NV) & 1);
+        TR(2, 5, gs);
         if (ahead) mbar_wait(&bar[B_KFULL + (gs + 2) % NK], ((gs + 2) / NK) & 1);
+        TR(2, 6, gs);
 #pragma unroll
         for (int tile = 0; tile < 2; ++tile) {
           if (j == 0) mbar_wait(&bar[B_OEMPTY + tile], (n & 1) ^ 1);

@@ -9,12 +9,19 @@
 //                             in TMEM (2 x 256 columns, double buffered)
 //   warps 2..5  epilogue:     tcgen05.ld 32x32b.x32 -> fused epilogue -> TMA store
 //
-// Two tile shapes share the code (template CG):
+// Tile shapes share the code (template CG):
 //   CG=1  128x256 tile per CTA, cta_group::1, 4-stage ring of 48 KB
 //   CG=2  256x256 tile per CTA pair (cluster of 2), cta_group::2: CTA r loads
 //         rows [r*128, r*128+128) of both the A and the B tile (32 KB per
 //         stage, 6 stages); the leader issues the MMAs, commits are multicast
 //         to both CTAs, both epilogues release the accumulator on the leader.
+//   CG=3  (default) 128x256 per CTA with cta_group::1 MMAs, clusters of 2
+//         M-adjacent CTAs: each loads its A tile and HALF of the shared weight
+//         tile, multicast into both CTAs (TMA .multicast::cluster); a stage is
+//         recycled when both CTAs' MMAs committed (multicast tcgen05.commit).
+//         L2->SM traffic per k-block 32 KB instead of 48 KB; on the power-capped
+//         B200 that is worth ~6% higher clocks (profiles/).
+//   CG=4  as CG=3 with clusters of 4 (slower; kept for A/B).
 //
 // Epilogues: RESIDUAL adds the accumulator into the f32 residual stream with a
 // TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add, the read-modify-write
@@ -52,6 +59,25 @@ template <> struct Cfg<2> {
   static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 128 * BK * 2;
   static constexpr int B_ROWS = 128;
 };
+// CG=3: cta_group::1 MMAs (128x256 per CTA) in a cluster of 2 M-adjacent CTAs
+// that share the weight tile: each CTA TMA-loads half of B (128 rows) and
+// multicasts it to both, so L2->SM traffic per tile drops from 48 to 32 KB
+// per k-block while every MMA still reads only local shared memory.
+template <> struct Cfg<3> {
+  static constexpr int TILE_M = 256, STAGES = 4, GROUP_M = 8;
+  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 256 * BK * 2;
+  static constexpr int B_ROWS = 128;
+};
+// CG=4: as CG=3 with clusters of 4 (each CTA loads a quarter of B): 24 KB of
+// L2->SM traffic per k-block instead of 48.
+template <> struct Cfg<4> {
+  static constexpr int TILE_M = 512, STAGES = 4, GROUP_M = 4;
+  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 256 * BK * 2;
+  static constexpr int B_ROWS = 64;
+};
+// CTAs per cluster: 1 (CG=1), 2 (cta_group::2 pair, or B multicast), 4 (B multicast)
+template <int CG> constexpr int cluster_size() { return CG == 1 ? 1 : CG == 4 ? 4 : 2; }
+template <int CG> constexpr bool multicast_b() { return CG >= 3; }
 template <int CG>
 constexpr int smem_bytes() {
   return Cfg<CG>::STAGES * (Cfg<CG>::A_BYTES + Cfg<CG>::B_BYTES) + 4 * STG_WARP_BYTES +
@@ -210,18 +236,25 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  constexpr bool CLUSTER = CG >= 2;            // launched as clusters
+  constexpr int MMA_CG = CG == 2 ? 2 : 1;      // cta_group of the MMA / TMEM ops
+  const uint32_t rank = CLUSTER ? cluster_rank() : 0;
   const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4 * CG); }
+    // CG=3: a stage is free only when BOTH CTAs' MMAs have read it (the peer
+    // multicasts its half of B into this CTA's buffer)
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], multicast_b<CG>() ? cluster_size<CG>() : 1);
+    }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4 * MMA_CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    if constexpr (CG == 1) {
+    if constexpr (MMA_CG == 1) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                        smem_u32(tmem_slot)) : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -233,7 +266,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync_all();
+  if constexpr (CLUSTER) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -241,7 +274,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int nk = K / BK;
-  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+  constexpr int CS = cluster_size<CG>();
+  constexpr uint16_t MC_MASK = (uint16_t)((1u << CS) - 1);
+  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
 
   if (warp == 0) {
     int stage = 0;
@@ -252,13 +287,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one_sync()) {
-          // all TMA bytes of the pair land on the leader's barrier
-          const uint32_t bar = CG == 2 ? mapa_rank(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
-          if (leader) mbar_expect_tx(&full[stage], CG * (C::A_BYTES + C::B_BYTES));
-          tma_load<CG>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
-                       mb * C::TILE_M + (int)rank * 128);
-          tma_load<CG>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
-                       nb * BN + (int)rank * C::B_ROWS);
+          if constexpr (multicast_b<CG>()) {
+            // own A rows; own slice of B multicast into every CTA's stage buffer
+            mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+            const uint32_t bar = smem_u32(&full[stage]);
+            tma_load<1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
+                        mb * C::TILE_M + (int)rank * 128);
+            tma_load_mc(sB + stage * C::B_BYTES + rank * (C::B_ROWS * BK * 2), &tmB, bar,
+                        kb * BK, nb * BN + (int)rank * C::B_ROWS, MC_MASK);
+          } else {
+            // all TMA bytes of the pair land on the leader's barrier
+            const uint32_t bar = CG == 2 ? mapa_rank(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
+            if (leader) mbar_expect_tx(&full[stage], CG * (C::A_BYTES + C::B_BYTES));
+            tma_load<CG>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
+                         mb * C::TILE_M + (int)rank * 128);
+            tma_load<CG>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
+                         nb * BN + (int)rank * C::B_ROWS);
+          }
         }
         __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -267,7 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // whole warp walks the schedule; one elected lane issues (descriptors stay
     // in uniform registers, no per-MMA elect loop)
-    if (leader) {
+    if (CG != 2 || leader) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -285,14 +330,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (elect_one_sync()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              mma_f16<CG>(d_tmem, dA + ((stage * C::A_BYTES + k * 32) >> 4),
-                          dB + ((stage * C::B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
-            mma_commit<CG>(&empty[stage]);
+              mma_f16<MMA_CG>(d_tmem, dA + ((stage * C::A_BYTES + k * 32) >> 4),
+                              dB + ((stage * C::B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+            if constexpr (multicast_b<CG>()) mma_commit_mc1(&empty[stage], MC_MASK);
+            else mma_commit<MMA_CG>(&empty[stage]);
           }
           __syncwarp();
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (elect_one_sync()) mma_commit<CG>(&tfull[acc]);
+        if (elect_one_sync()) mma_commit<MMA_CG>(&tfull[acc]);
         __syncwarp();
       }
     }
@@ -335,10 +381,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync_all();
+  if constexpr (CLUSTER) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    if constexpr (CG == 1)
+    if constexpr (MMA_CG == 1)
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     else
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
@@ -395,8 +441,9 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
     attr = true;
   }
   const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + BN - 1) / BN);
-  const int slots = (device_sm_count() / CG) * CG;
-  const int grid = std::min(CG * tiles, slots);
+  constexpr int CS = cluster_size<CG>();
+  const int slots = (device_sm_count() / CS) * CS;
+  const int grid = std::min(CS * tiles, slots);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
@@ -404,13 +451,13 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.x = CS;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, CG>, ma, mb, mo, M, N, K, idesc, group_m, ep);
-  return check_launch(CG == 2 ? "gemm_tcgen05_2cta" : "gemm_tcgen05");
+  return check_launch(CG == 2 ? "gemm_tcgen05_2cta" : CG >= 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
 }
 
 }  // namespace tc
@@ -428,15 +475,19 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (ep.kind == KRR_EPI_QKV_ROPE && ep.qkv.head_dim % 32 != 0)
     return launch_gemm_simt(act_dtype, A, B, M, N, K, ep, s);  // a chunk must stay in one head
 
-  // Tile shape: KRR_GEMM_CTA=1 (128x256 per CTA) | 2 (256x256 per CTA pair,
-  // cta_group::2) | 3 = per-shape choice (2 for K <= 4096, 1 for the deep-K
-  // down projection).  Read once per process; default 1 (measured best overall
-  // on the power-capped C3 step).
+  // Tile shape (KRR_GEMM_CTA, read once per process):
+  //   1  128x256 per CTA, no cluster
+  //   2  256x256 per CTA pair (cta_group::2)
+  //   3  per-shape 2 / 1
+  //   4  128x256 per CTA, clusters of 2 M-adjacent CTAs sharing the weight tile
+  //      by TMA multicast (DEFAULT: 2/3 of the L2->SM traffic of mode 1; under
+  //      the power cap this buys ~6% higher clocks, +6% pairs/s on C3)
+  //   5  as 4 with clusters of 4 (measured much slower)
   static int env_mode = -1;
   if (env_mode < 0) {
     const char* e = getenv("KRR_GEMM_CTA");
-    env_mode = e ? atoi(e) : 1;
-    if (env_mode < 1 || env_mode > 3) env_mode = 1;
+    env_mode = e ? atoi(e) : 4;
+    if (env_mode < 1 || env_mode > 5) env_mode = 4;
   }
   const int mode = env_mode == 3 ? (K <= 4096 && M >= 1024 ? 2 : 1) : env_mode;
   const CUtensorMapDataType dt =
@@ -445,7 +496,8 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   CUtensorMap ma, mb, mo;
   int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK, mode == 2 ? 128 : 256,
+  rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK,
+                mode == 5 ? 64 : (mode == 2 || mode == 4) ? 128 : 256,
                 CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   if (ep.kind == KRR_EPI_RESIDUAL) {
@@ -464,10 +516,14 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)(tile_m >> 4) << 24);
   if (act_dtype == KRR_F16)
-    return mode == 2 ? launch<__half, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
-                     : launch<__half, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
-  return mode == 2 ? launch<__nv_bfloat16, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
-                   : launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
+    return mode == 2   ? launch<__half, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
+           : mode == 4 ? launch<__half, 3>(ma, mb, mo, M, N, K, idesc, ep, s)
+           : mode == 5 ? launch<__half, 4>(ma, mb, mo, M, N, K, idesc, ep, s)
+                       : launch<__half, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
+  return mode == 2   ? launch<__nv_bfloat16, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
+         : mode == 4 ? launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, ep, s)
+         : mode == 5 ? launch<__nv_bfloat16, 4>(ma, mb, mo, M, N, K, idesc, ep, s)
+                     : launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
 }
 
 }  // namespace krr

@@ -442,10 +442,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   }
   const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + BN - 1) / BN);
   constexpr int CS = cluster_size<CG>();
-  const int slots = (device_sm_count() / CS) * CS;
-  const int grid = std::min(CS * tiles, slots);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
@@ -456,6 +453,21 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
+  // persistent grid: as many clusters as can be co-resident (GPC boundaries
+  // can leave SMs unusable for larger clusters), queried once per shape class
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    cfg.gridDim = dim3((device_sm_count() / CS) * CS);
+    int n = 0;
+    if (CS > 1 && cudaOccupancyMaxActiveClusters(&n, gemm_tcgen05_kernel<T, CG>, &cfg) == cudaSuccess &&
+        n > 0)
+      max_clusters = n;
+    else
+      max_clusters = device_sm_count() / CS;
+    cudaGetLastError();
+  }
+  const int grid = std::min(CS * tiles, CS * max_clusters);
+  cfg.gridDim = dim3(grid);
   cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, CG>, ma, mb, mo, M, N, K, idesc, group_m, ep);
   return check_launch(CG == 2 ? "gemm_tcgen05_2cta" : CG >= 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
 }

@@ -13,7 +13,7 @@ timeout -s KILL 1200 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_dura
 echo "ncu list rc=$?"
 timeout -s KILL 1200 ncu --nvtx --nvtx-include "timed/" --set full --clock-control none --import-source on -k regex:"gemm_tcgen05" -s 2 -c 1 -o gpurun_out/${TAG}_gemm_full $CMD > gpurun_out/${TAG}_gemm_full.log 2>&1
 echo "ncu gemm rc=$?"
-timeout -s KILL 900 ncu --nvtx --nvtx-include "timed/" --set full --clock-control none --import-source on -k regex:"attn_pp" -c 1 -o gpurun_out/${TAG}_attn_full $CMD > gpurun_out/${TAG}_attn_full.log 2>&1
+timeout -s KILL 900 ncu --nvtx --nvtx-include "timed/" --set full --clock-control none --import-source on -k regex:"attn_(fa|pp|tc)" -c 1 -o gpurun_out/${TAG}_attn_full $CMD > gpurun_out/${TAG}_attn_full.log 2>&1
 echo "ncu attn rc=$?"
 timeout -s KILL 1500 python bench.py --config c4 --steps 3 --warmup 2 --latency-reps 5 --no-cpu-baseline > gpurun_out/${TAG}_c4.json 2> gpurun_out/${TAG}_c4.err
 echo "c4 rc=$?"; python scripts/show.py gpurun_out/${TAG}_c4.json; tail -2 gpurun_out/${TAG}_c4.err

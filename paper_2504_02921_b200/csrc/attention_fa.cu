@@ -43,7 +43,7 @@ __device__ unsigned long long g_fa_trace[16 * 8 * 64];
 constexpr int TM = 128;
 constexpr int KB = 64;
 constexpr int NK = 4, NV = 4;   // K / V ring depth
-constexpr int THREADS = 352;    // w0 producers (lanes 0 Q, 1 K, 2 V), w1 / w10 MMA (tile A / B), w2-5 / w6-9 softmax
+constexpr int THREADS = 320;    // w0 producers (lanes 0 Q, 1 K, 2 V), w1 MMA, w2-5 / w6-9 softmax
 constexpr float RESCALE_LOG2 = 15.0f;   // P <= 2^15 < f16 max
 
 struct Params {
@@ -139,9 +139,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmPre)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur)) : "memory");
     mbar_init(&bar[B_QFULL], 1);
-    mbar_init(&bar[B_QEMPTY], 2);                       // both tiles' MMA warps release
-    for (int s = 0; s < NK; ++s) { mbar_init(&bar[B_KFULL + s], 1); mbar_init(&bar[B_KEMPTY + s], 2); }
-    for (int s = 0; s < NV; ++s) { mbar_init(&bar[B_VFULL + s], 1); mbar_init(&bar[B_VEMPTY + s], 2); }
+    mbar_init(&bar[B_QEMPTY], 1);
+    for (int s = 0; s < NK; ++s) { mbar_init(&bar[B_KFULL + s], 1); mbar_init(&bar[B_KEMPTY + s], 1); }
+    for (int s = 0; s < NV; ++s) { mbar_init(&bar[B_VFULL + s], 1); mbar_init(&bar[B_VEMPTY + s], 1); }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&bar[B_SFULL + i], 1);
       mbar_init(&bar[B_PFULL + i], 4);
@@ -209,66 +209,88 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp == 1 || warp == 10) {
-    // ---------------------------------------------------------- MMA issuers
-    // One warp per tile (warp 1: tile A, warp 10: tile B), so a tile waiting
-    // for its softmax never holds back the other tile's MMAs.  Each stream
-    // keeps its own PV(j) -> S(j+2) order (in-order pipe per issuing thread);
-    // shared K/V/Q stages are released by two commits (barrier count 2).
-    const int tile = warp == 1 ? 0 : 1;
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
     constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
     constexpr uint32_t idesc_s = (1u << 4) | (fmt << 7) | (fmt << 10) |
                                  ((uint32_t)(KB >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
     constexpr uint32_t idesc_o = (1u << 4) | (fmt << 7) | (fmt << 10) | (1u << 16) |
                                  ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
-    const uint64_t dQ = sw128_desc(smem_u32(sQ + tile * S::Q_TILE));
+    const uint64_t dQ = sw128_desc(smem_u32(sQ));
     const uint64_t dK = sw128_desc(smem_u32(sK));
     const uint64_t dV = sw128_desc_mn(smem_u32(sV), S::ATOM_KV, 1024);
-    const uint32_t t_s = tmem + tile * 256, t_o = tmem + tile * 256 + 2 * KB;
     int g = 0, n = 0;
-    // S(gs) = Q . K(gs)^T into S buffer gs&1; releases the K stage (one of two arrivals)
-    auto issue_s = [&](int gs, bool last_s) {
+    // S_tile(gs) = Q_tile . K(gs)^T into S buffer gs&1
+    auto issue_s = [&](int tile, int gs) {
       const int st = gs % NK;
-      mbar_wait(&bar[B_KFULL + st], (gs / NK) & 1);
-      tc_fence_after();
       if (elect_one_sync()) {
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t qoff = (k >> 2) * S::ATOM_Q + (k & 3) * 32;
+          const uint32_t qoff = tile * S::Q_TILE + (k >> 2) * S::ATOM_Q + (k & 3) * 32;
           const uint32_t koff = st * S::KV_BYTES + (k >> 2) * S::ATOM_KV + (k & 3) * 32;
-          mma_f16<1>(t_s + (gs & 1) * KB, dQ + (qoff >> 4), dK + (koff >> 4), idesc_s, k > 0);
+          mma_f16<1>(tmem + tile * 256 + (gs & 1) * KB, dQ + (qoff >> 4), dK + (koff >> 4),
+                     idesc_s, k > 0);
         }
         mma_commit<1>(&bar[B_SFULL + tile * 2 + (gs & 1)]);
-        mma_commit<1>(&bar[B_KEMPTY + st]);
-        if (last_s) mma_commit<1>(&bar[B_QEMPTY]);        // Q no longer read by this item
+      }
+      __syncwarp();
+    };
+    // O_tile += P_tile(gs) . V(gs), P in the first KB/2 columns of S buffer gs&1
+    auto issue_pv = [&](int tile, int gs, bool acc) {
+      const int sv = gs % NV;
+      if (elect_one_sync()) {
+#pragma unroll
+        for (int k = 0; k < KB / 16; ++k)
+          mma_ts(tmem + tile * 256 + 2 * KB, tmem + tile * 256 + (gs & 1) * KB + k * 8,
+                 dV + ((sv * S::KV_BYTES + k * 16 * 128) >> 4), idesc_o, acc || k > 0);
+        mma_commit<1>(&bar[B_PVDONE + tile * 2 + (gs & 1)]);
+      }
+      __syncwarp();
+    };
+    auto issue_s_pair = [&](int gs, bool last_s) {     // S(gs) for both tiles, release K
+      mbar_wait(&bar[B_KFULL + gs % NK], (gs / NK) & 1);
+      tc_fence_after();
+      issue_s(0, gs);
+      issue_s(1, gs);
+      if (elect_one_sync()) {
+        mma_commit<1>(&bar[B_KEMPTY + gs % NK]);
+        if (last_s) mma_commit<1>(&bar[B_QEMPTY]);      // Q no longer read by this item
       }
       __syncwarp();
     };
     for (int it = blockIdx.x; it < p.items; it += gridDim.x, ++n) {
       const Item x = item_of(p, it);
       mbar_wait(&bar[B_QFULL], n & 1);
-      issue_s(g, x.nb == 1);
-      if (x.nb > 1) issue_s(g + 1, x.nb == 2);
+      issue_s_pair(g, x.nb == 1);
+      if (x.nb > 1) issue_s_pair(g + 1, x.nb == 2);
       for (int j = 0; j < x.nb; ++j) {
-        const int gs = g + j, sv = gs % NV;
-        mbar_wait(&bar[B_VFULL + sv], (gs / NV) & 1);
-        if (j == 0) mbar_wait(&bar[B_OEMPTY + tile], (n & 1) ^ 1);
-        mbar_wait(&bar[B_PFULL + tile * 2 + (gs & 1)], (gs >> 1) & 1);
-        TR(2, tile * 2, gs);
-        tc_fence_after();
-        if (elect_one_sync()) {        // O += P(gs) . V(gs), P = TMEM A operand
+        const int gs = g + j;
+        const bool ahead = j + 2 < x.nb;
+        TR(2, 4, gs);
+        mbar_wait(&bar[B_VFULL + gs % NV], (gs / NV) & 1);
+        TR(2, 5, gs);
+        if (ahead) mbar_wait(&bar[B_KFULL + (gs + 2) % NK], ((gs + 2) / NK) & 1);
+        TR(2, 6, gs);
 #pragma unroll
-          for (int k = 0; k < KB / 16; ++k)
-            mma_ts(t_o, t_s + (gs & 1) * KB + k * 8,
-                   dV + ((sv * S::KV_BYTES + k * 16 * 128) >> 4), idesc_o, j > 0 || k > 0);
-          mma_commit<1>(&bar[B_PVDONE + tile * 2 + (gs & 1)]);
-          mma_commit<1>(&bar[B_VEMPTY + sv]);
-          if (j == x.nb - 1) mma_commit<1>(&bar[B_ODONE + tile]);
+        for (int tile = 0; tile < 2; ++tile) {
+          if (j == 0) mbar_wait(&bar[B_OEMPTY + tile], (n & 1) ^ 1);
+          mbar_wait(&bar[B_PFULL + tile * 2 + (gs & 1)], (gs >> 1) & 1);
+          TR(2, tile * 2, gs);
+          tc_fence_after();
+          issue_pv(tile, gs, j > 0);
+          if (ahead) issue_s(tile, gs + 2);   // in-order pipe: PV(gs) reads P before S(gs+2) lands
+          else if (j == x.nb - 1 && elect_one_sync()) mma_commit<1>(&bar[B_ODONE + tile]);
+          __syncwarp();
+          TR(2, tile * 2 + 1, gs);
+        }
+        if (elect_one_sync()) {
+          mma_commit<1>(&bar[B_VEMPTY + gs % NV]);
+          if (ahead) {
+            mma_commit<1>(&bar[B_KEMPTY + (gs + 2) % NK]);
+            if (j + 2 == x.nb - 1) mma_commit<1>(&bar[B_QEMPTY]);
+          }
         }
         __syncwarp();
-        // in-order pipe: PV(gs) reads P before S(gs+2) lands in the same columns
-        if (j + 2 < x.nb) issue_s(gs + 2, j + 2 == x.nb - 1);
-        TR(2, tile * 2 + 1, gs);
       }
       g += x.nb;
     }

@@ -317,7 +317,16 @@ static unsigned grid_for(int64_t n, int threads) {
 
 static int do_gemm(int backend, int act, const void* A, const void* B, int64_t M, int N, int K,
                    const EpiParams& ep, cudaStream_t s) {
-  if (backend == KRR_GEMM_AUTO) backend = (act == KRR_F32) ? KRR_GEMM_SIMT : KRR_GEMM_TCGEN05;
+  if (backend == KRR_GEMM_AUTO) {
+    // tensor cores for 16-bit operands whenever the tile constraints hold
+    // (K % 64, N % 32, 16-byte aligned operands); CUDA-core kernel otherwise
+    // (e.g. the reference's default desk config, d=128 with 16-wide heads, is
+    // fine; odd widths are not)
+    const bool tc_ok = act != KRR_F32 && K % 64 == 0 && N % 32 == 0 &&
+                       (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+    backend = tc_ok ? KRR_GEMM_TCGEN05 : KRR_GEMM_SIMT;
+  }
   ProfScope ps(s, 0, 2.0 * (double)M * N * K);
   if (backend == KRR_GEMM_TCGEN05) return launch_gemm_tcgen05(act, A, B, M, N, K, ep, s);
   return launch_gemm_simt(act, A, B, M, N, K, ep, s);
@@ -325,8 +334,10 @@ static int do_gemm(int backend, int act, const void* A, const void* B, int64_t M
 
 static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t s) {
   if (backend == KRR_ATTN_AUTO) {
+    const bool mma_hd = p.head_dim == 64 || p.head_dim == 128 || p.head_dim == 256;
     if (act == KRR_F32) backend = KRR_ATTN_SIMT;
-    else backend = attention_tcgen05_supported(act, p) ? KRR_ATTN_TCGEN05 : KRR_ATTN_MMA;
+    else if (attention_tcgen05_supported(act, p)) backend = KRR_ATTN_TCGEN05;
+    else backend = mma_hd ? KRR_ATTN_MMA : KRR_ATTN_SIMT;   // any other head_dim
   }
   ProfScope ps(s, 1);
   if (backend == KRR_ATTN_TCGEN05) {

@@ -10,6 +10,7 @@ prefix KV read straight from pool slots.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -19,6 +20,18 @@ from .kvpool import KVPool
 from .model import DeviceWeights
 
 DEFAULT_WORKSPACE_BUDGET = 32 << 30  # bytes of activations per krr_forward call
+
+# The reference calls score_* from several rerank worker threads at once
+# (pipeline.py:375-379, 488-504).  Device scratch (workspace,
+# suffix KV) is shared per device, so device passes are serialised per device;
+# the GPU executes them back to back anyway.
+_DEVICE_LOCKS: dict = {}
+_LOCKS_GUARD = threading.Lock()
+
+
+def device_lock(device) -> threading.RLock:
+    with _LOCKS_GUARD:
+        return _DEVICE_LOCKS.setdefault(str(device), threading.RLock())
 
 
 class _Workspace:
@@ -104,6 +117,11 @@ def prefill_slots(w: DeviceWeights, pool: KVPool, slots, doc_tokens, valid_len,
     """Document prefill (reranker.py:182-201) of n docs straight into pool
     slots: positions [0, D), pad rows computed and kept, K/V written by the
     QKV epilogue into the slot pages."""
+    with device_lock(w.device):
+        _prefill_slots(w, pool, slots, doc_tokens, valid_len, max_rows)
+
+
+def _prefill_slots(w, pool, slots, doc_tokens, valid_len, max_rows):
     import torch
     if pool.code != w.code:
         raise ConfigError(f"pool dtype {pool.dtype} != weights dtype {w.dtype}")
@@ -151,6 +169,11 @@ def score_slots(w: DeviceWeights, pool: KVPool, slots, q_tokens, q_valid=None, l
     """Score pairs (pool slot, query tokens) on the device; returns f32 [n] on device.
 
     slots int [n] (host or device), q_tokens int [n, Q] (host or device)."""
+    with device_lock(w.device):
+        return _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out)
+
+
+def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out):
     import torch
     if pool.code != w.code:
         raise ConfigError(f"pool dtype {pool.dtype} != weights dtype {w.dtype}")

@@ -214,3 +214,58 @@ def test_yes_no_head_is_two_row_logit_difference(c1_golden):
                                       np.concatenate([np.arange(D) < vl, q != 0]))
         want = float(hidden[int(np.nonzero(q != 0)[0][-1])] @ v)
         assert abs(r.score - want) <= 1e-4 * max(1.0, abs(want))
+
+
+@pytest.mark.parametrize("cfg,lay", [
+    (ModelConfig(), LayoutConfig()),                       # reference default desk config (HD=16)
+    (ModelConfig(layers=2, model_dim=96, heads=3, kv_heads=3, head_dim=32),
+     LayoutConfig(document_len=70, query_len=20)),         # MHA, odd widths -> CUDA-core paths
+    (ModelConfig(layers=2, model_dim=192, heads=3, kv_heads=1, head_dim=64),
+     LayoutConfig(document_len=100, query_len=33)),        # G=3, ragged tiles
+])
+@pytest.mark.parametrize("precision", ["f32", "f16"])
+def test_other_configs_vs_oracle(cfg, lay, precision):
+    """Any ModelConfig the reference accepts runs (tensor-core kernels where the
+    shape allows, CUDA-core kernels otherwise) and matches the oracle."""
+    import oracle
+    rng = np.random.default_rng(3)
+    D, Q = lay.document_len, lay.query_len
+    docs = rng.integers(1, cfg.vocab_size, (4, D))
+    docs[1, D - 9:] = 0
+    qs = rng.integers(1, cfg.vocab_size, (4, Q))
+    qs[2, Q - 4:] = 0
+    model = krr.RerankModel.build(cfg, lay, precision=precision)
+    kvs = krr.doc_prefill_batch(model, docs, [f"o{i}" for i in range(4)])
+    res, _ = krr.score_batch(model, [("q", k.chunk_id, k, q) for k, q in zip(kvs, qs)], "reuse")
+    s = np.array([r.score for r in res])
+    ow = oracle.init_weights(oracle.OracleConfig(
+        layers=cfg.layers, model_dim=cfg.model_dim, heads=cfg.heads, kv_heads=cfg.kv_heads,
+        head_dim=cfg.head_dim, vocab_size=cfg.vocab_size, max_position=cfg.max_position,
+        document_len=D, query_len=Q))
+    if precision == "f16":
+        ow = oracle.round_weights(ow)
+    ref = np.array([oracle.score_full(ow, docs[i], qs[i]) for i in range(4)])
+    if precision == "f32":
+        assert rel_err(s, ref) <= F32_TOL, rel_err(s, ref)
+    else:
+        assert normwise(s, ref) <= F16_NORMWISE, normwise(s, ref)
+
+
+def test_concurrent_score_batch_threads(c1_golden, model_f16):
+    """score_batch from several threads at once (the reference's rerank
+    workers) gives the same scores as one call."""
+    import threading
+    docs, q = c1_golden["doc_tokens"][:12], c1_golden["query_tokens"]
+    kvs = krr.doc_prefill_batch(model_f16, docs, [f"t{i}" for i in range(12)])
+    want, _ = krr.score_batch(model_f16, [("q", k.chunk_id, k, q) for k in kvs], "reuse")
+    got = [None] * 4
+
+    def work(i):
+        got[i], _ = krr.score_batch(model_f16, [("q", k.chunk_id, k, q) for k in kvs], "reuse")
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for g in got:
+        assert [r.score for r in g] == [r.score for r in want]

@@ -35,6 +35,7 @@
 // (SPEC.md:178 batch invariance).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 #include "epilogue.cuh"
@@ -97,8 +98,22 @@ __device__ __forceinline__ float gelu_fast(float x) {
 }
 
 template <int CG>
+// Raster: GM > 0 -> groups of GM m-tiles sweep all n-tiles (the activation
+// panels of a group stay in L2); GM < 0 -> bands of -GM n-tiles sweep all
+// m-tiles (a weight band stays in L2 and is read from DRAM once).
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int GM, int& mb,
                                             int& nb) {
+  if (GM < 0) {
+    const int GN = -GM;
+    const int per_band = GN * num_m;
+    const int band = tile / per_band;
+    const int first_n = band * GN;
+    const int bsize = min(num_n - first_n, GN);
+    const int r = tile - band * per_band;
+    nb = first_n + r % bsize;
+    mb = r / bsize;
+    return;
+  }
   const int per_group = GM * num_n;
   const int group = tile / per_group;
   const int first_m = group * GM;
@@ -429,10 +444,27 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
                   int N, int K, uint32_t idesc, const EpiParams& ep, cudaStream_t s) {
   // L2 rasterisation: GROUP_M m-tiles share each weight (B) panel while it is
   // L2-resident (KRR_GEMM_GROUP_M overrides, fixed per process).
-  static int group_m = -1;
-  if (group_m < 0) {
+  static int group_m_env = -1, raster = -1;
+  if (group_m_env < 0) {
     const char* e = getenv("KRR_GEMM_GROUP_M");
-    group_m = (e && atoi(e) > 0) ? atoi(e) : Cfg<CG>::GROUP_M;
+    group_m_env = (e && atoi(e) > 0) ? atoi(e) : Cfg<CG>::GROUP_M;
+    // m (default) | n | auto: N-bands cut DRAM reads (MLP-up 22.8 -> ~10 GB per
+    // launch) but measured ~1% slower on the power-capped C3 step
+    const char* r = getenv("KRR_GEMM_RASTER");
+    raster = !r ? 0 : (r[0] == 'm' ? 0 : r[0] == 'n' ? 1 : 2);
+  }
+  // DRAM traffic model: M-groups re-read the weight once per group
+  // (|A| + |B|*num_m/GM); N-bands re-read the activations once per band
+  // (|A|*num_n/GN + |B|) with the band (GN x 256 x K x 2 B) held in L2.
+  int group_m = group_m_env;
+  {
+    const double A = (double)M * K * 2, B = (double)N * K * 2;
+    const int num_m = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M), num_n = (N + BN - 1) / BN;
+    int gn = (int)((40.0 * (1 << 20)) / (256.0 * K * 2));      // ~40 MB weight band
+    gn = std::max(1, std::min(gn, num_n));
+    const double cost_m = A + B * std::max(1.0, (double)num_m / group_m_env);
+    const double cost_n = A * std::ceil((double)num_n / gn) + B;
+    if (raster == 1 || (raster == 2 && cost_n < 0.7 * cost_m)) group_m = -gn;
   }
   constexpr int SMEM = smem_bytes<CG>();
   static bool attr = false;

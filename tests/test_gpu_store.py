@@ -252,3 +252,27 @@ def test_quantised_host_tier_matches_hrkv_entries(model16, quant, scheme):
     want = engine.score_slots(model16.weights, ref_pool, np.array(ref_slots)[pair_doc], q)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+def test_host_dockv_from_reference_entry_scores(g, model32, model16):
+    """Reference-style usage: decode_entry() gives a host f32 DocKV (zero-copy
+    view over the HRKV bytes) and score_reuse / score_batch stage it into HBM;
+    f32 debug build matches the oracle, f16 path within the 16-bit gate, and a
+    mixed batch (host + device DocKVs) scores each pair like its single call."""
+    data = g["entry_f32"].tobytes()
+    dkv = codec.decode_entry(data)
+    assert isinstance(dkv.kv, krr.KVTensorSet) and dkv.valid_len == 90
+    q = np.random.default_rng(8).integers(1, 32768, 48)
+    w = oracle.init_weights(oracle.OracleConfig(layers=2, model_dim=256, heads=4, kv_heads=2,
+                                                head_dim=64, vocab_size=32768,
+                                                document_len=128, query_len=48))
+    ref = oracle.score_reuse(w, dkv.kv.keys, dkv.kv.values, dkv.valid_len, q)
+    s32, c = krr.score_reuse(model32, dkv, q)
+    assert abs(s32 - ref) <= 1e-4 * max(1.0, abs(ref))
+    assert c.kv_bytes_loaded == 262144 and c.linear_token_count == 48
+    s16, _ = krr.score_reuse(model16, dkv, q)
+    assert abs(s16 - ref) <= 2e-2 * max(1.0, abs(ref))
+    dev = krr.doc_prefill(model16, g["doc_tokens"], "dev")
+    res, _ = krr.score_batch(model16, [("q", "h", dkv, q), ("q", "dev", dev, q)], "reuse")
+    assert res[0].score == s16
+    assert res[1].score == krr.score_reuse(model16, dev, q)[0]

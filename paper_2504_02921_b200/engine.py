@@ -324,3 +324,48 @@ def run_layers(w: DeviceWeights, l0: int, l1: int, tokens, tok_valid, pos0: int,
                    _ptr(x_in), _ptr(x_out))
     stream = torch.cuda.current_stream(w.device).cuda_stream
     _lib.check(_lib.lib().krr_forward(C.byref(m), C.byref(b), ws.data_ptr(), ws.numel(), stream))
+
+
+class GraphedScorer:
+    """CUDA-graph replay of one scoring pass (krr_forward over n pairs of query
+    length Q + per-query top-k) for a fixed batch shape, for latency-critical
+    serving: the ~7 launches per layer and the host-side argument marshalling
+    are recorded once; a call is two small H2D copies, one graph launch and a
+    D2H of the top-k.  Inputs are copied into static device buffers."""
+
+    def __init__(self, w: DeviceWeights, pool: KVPool, n_q: int, n_c: int, Q: int, k: int):
+        import torch
+        self.w, self.pool, self.n_q, self.n_c, self.Q, self.k = w, pool, n_q, n_c, Q, k
+        dev = w.device
+        n = n_q * n_c
+        self.slots = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.q = torch.ones((n_q, Q), dtype=torch.int32, device=dev)
+        self.ids = torch.arange(n, dtype=torch.int32, device=dev)
+        self.qidx = torch.arange(n_q, device=dev).repeat_interleave(n_c)
+        self.scores = torch.empty(n, dtype=torch.float32, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(self.stream):
+            for _ in range(2):                    # warm-up: workspace, descriptors, attributes
+                self._body()
+        torch.cuda.current_stream(dev).wait_stream(self.stream)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self.out_idx, self.out_sc = self._body()
+
+    def _body(self):
+        score_slots(self.w, self.pool, self.slots, self.q.index_select(0, self.qidx),
+                    out=self.scores, max_rows=self.n_q * self.n_c * self.Q)
+        return segmented_topk(self.scores, self.ids, self.n_q, self.n_c, self.k)
+
+    def __call__(self, slots, q_tokens, doc_ids):
+        """slots int [n_q*n_c], q_tokens int [n_q, Q], doc_ids int [n_q*n_c] (host);
+        returns (idx, scores) host arrays [n_q, k] (idx = position within the query's
+        candidates)."""
+        import torch
+        self.slots.copy_(torch.as_tensor(np.asarray(slots, np.int64)), non_blocking=True)
+        self.q.copy_(torch.as_tensor(np.asarray(q_tokens, np.int32)), non_blocking=True)
+        self.ids.copy_(torch.as_tensor(np.asarray(doc_ids, np.int32)), non_blocking=True)
+        self.graph.replay()
+        return self.out_idx.cpu().numpy(), self.out_sc.cpu().numpy()

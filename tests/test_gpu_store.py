@@ -276,3 +276,25 @@ def test_host_dockv_from_reference_entry_scores(g, model32, model16):
     res, _ = krr.score_batch(model16, [("q", "h", dkv, q), ("q", "dev", dev, q)], "reuse")
     assert res[0].score == s16
     assert res[1].score == krr.score_reuse(model16, dev, q)[0]
+
+
+def test_graphed_scorer_matches_eager(model16):
+    """CUDA-graph replay of the scoring pass gives the eager scores and top-k,
+    and picks up new inputs on every replay."""
+    rng = np.random.default_rng(9)
+    docs = rng.integers(1, 32768, (6, 128))
+    pool = krr.KVPool(C1[0], 128, 6, "f16")
+    slots = pool.allocate([f"g{i}" for i in range(6)])
+    engine.prefill_slots(model16.weights, pool, slots, docs, np.full(6, 128))
+    gs = engine.GraphedScorer(model16.weights, pool, 2, 6, 48, 3)
+    for trial in range(2):
+        q = rng.integers(1, 32768, (2, 48))
+        perm = np.stack([rng.permutation(6) for _ in range(2)])
+        sl = slots[perm].reshape(-1)
+        idx, sc = gs(sl, q, perm.reshape(-1))
+        want = engine.score_slots(model16.weights, pool, sl, np.repeat(q, 6, axis=0)).cpu().numpy()
+        for qi in range(2):
+            seg = want[qi * 6:(qi + 1) * 6]
+            order = sorted(range(6), key=lambda j: (-seg[j], perm[qi, j]))[:3]
+            assert idx[qi].tolist() == order
+            assert np.array_equal(sc[qi], seg[order])

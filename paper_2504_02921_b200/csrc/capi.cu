@@ -309,6 +309,54 @@ __global__ void dequant_pages_kernel(const uint8_t* __restrict__ codes,
   }
 }
 
+// Vectorised form for the streaming path (host tier -> staging, once per
+// document per step): one thread expands 16 consecutive codes of one row
+// (16-byte / 8-byte code load, 16 channel scales, 32/64-byte store); grid.y
+// walks (tensor, kv_head) so no 64-bit division per element.  Same per-element
+// arithmetic as dequant_pages_kernel (f32 code*scale, then round to T).
+template <typename T, int BITS>
+__global__ void __launch_bounds__(256) dequant_pages_vec_kernel(
+    const uint8_t* __restrict__ codes, const float* __restrict__ scales, int KVH, int D, int HD,
+    T* __restrict__ out) {
+  const int th = blockIdx.y;                    // t * KVH + h
+  const int t = th / KVH, h = th - t * KVH;
+  const int64_t te = (int64_t)KVH * D * HD;
+  const int64_t tb = BITS == 8 ? te : te / 2;
+  const int chunks = D * HD / 16;               // per (tensor, head)
+  const int64_t head0 = (int64_t)h * D * HD;    // element offset of the head in its tensor
+  const float* sc = scales + (int64_t)th * HD;
+  T* o = out + t * te + head0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < chunks; j += gridDim.x * blockDim.x) {
+    const int e = j * 16;
+    const int c = e % HD;
+    int q[16];
+    if constexpr (BITS == 8) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(codes + t * tb + head0 + e));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) q[i] = (int)(int8_t)(w[i >> 2] >> (8 * (i & 3)));
+    } else {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(codes + t * tb + (head0 + e) / 2));
+      const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) q[i] = (int)(((w[i >> 3] >> (4 * (i & 7))) & 0xF) ^ 8) - 8;
+    }
+    alignas(16) T r[16];
+#pragma unroll
+    for (int i = 0; i < 16; i += 4) {
+      const float4 s4 = __ldg(reinterpret_cast<const float4*>(sc + c + i));
+      r[i + 0] = Act<T>::from((float)q[i + 0] * s4.x);
+      r[i + 1] = Act<T>::from((float)q[i + 1] * s4.y);
+      r[i + 2] = Act<T>::from((float)q[i + 2] * s4.z);
+      r[i + 3] = Act<T>::from((float)q[i + 3] * s4.w);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(o + e);
+    const uint4* srcv = reinterpret_cast<const uint4*>(r);
+#pragma unroll
+    for (int i = 0; i < (int)(16 * sizeof(T) / 16); ++i) dst[i] = srcv[i];
+  }
+}
+
 static unsigned grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   const int64_t cap = (int64_t)device_sm_count() * 32;
@@ -554,6 +602,22 @@ int krr_dequant_pages(const uint8_t* codes, const float* scales, int32_t bits, i
   KRR_REQUIRE(bits == 8 || bits == 4, KRR_ECONFIG, "dequant bits must be 8 or 4");
   if (n_tensors == 0) return KRR_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  const bool vec = head_dim % 16 == 0 && (reinterpret_cast<uintptr_t>(codes) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(scales) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                   (int64_t)n_tensors * kv_heads <= 65535;
+  if (vec) {
+    const int chunks = doc_len * head_dim / 16;
+    const dim3 grid((unsigned)std::max(1, std::min((chunks + 255) / 256, 64)),
+                    (unsigned)(n_tensors * kv_heads));
+#define KRR_DQ(T, B) \
+  dequant_pages_vec_kernel<T, B><<<grid, 256, 0, s>>>(codes, scales, kv_heads, doc_len, head_dim, (T*)out)
+    if (out_dtype == KRR_F32) { if (bits == 8) KRR_DQ(float, 8); else KRR_DQ(float, 4); }
+    else if (out_dtype == KRR_F16) { if (bits == 8) KRR_DQ(__half, 8); else KRR_DQ(__half, 4); }
+    else { if (bits == 8) KRR_DQ(__nv_bfloat16, 8); else KRR_DQ(__nv_bfloat16, 4); }
+#undef KRR_DQ
+    return check_launch("dequant_pages");
+  }
   const unsigned g = grid_for((int64_t)n_tensors * kv_heads * doc_len * head_dim, 256);
   if (out_dtype == KRR_F32)
     dequant_pages_kernel<float><<<g, 256, 0, s>>>(codes, scales, n_tensors, bits, kv_heads,

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmOut, int64_t M, int N, int K,
-                        uint32_t idesc, int group_m, EpiParams ep) {
+                        uint32_t idesc, int group_m, int bn, EpiParams ep) {
   using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -286,7 +286,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_m = (int)((M + C::TILE_M - 1) / C::TILE_M);
-  const int num_n = (N + BN - 1) / BN;
+  // bn = N-tile width (256, or 128 for narrow layers, CG=1/3 only); the smem
+  // ring and TMEM are sized for 256
+  const int num_n = (N + bn - 1) / bn;
   const int tiles = num_m * num_n;
   const int nk = K / BK;
   constexpr int CS = cluster_size<CG>();
@@ -304,20 +306,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (elect_one_sync()) {
           if constexpr (multicast_b<CG>()) {
             // own A rows; own slice of B multicast into every CTA's stage buffer
-            mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+            const int b_rows = bn / CS;                 // this CTA's slice of the weight tile
+            mbar_expect_tx(&full[stage], C::A_BYTES + bn * BK * 2);
             const uint32_t bar = smem_u32(&full[stage]);
             tma_load<1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
                         mb * C::TILE_M + (int)rank * 128);
-            tma_load_mc(sB + stage * C::B_BYTES + rank * (C::B_ROWS * BK * 2), &tmB, bar,
-                        kb * BK, nb * BN + (int)rank * C::B_ROWS, MC_MASK);
+            tma_load_mc(sB + stage * C::B_BYTES + rank * (b_rows * BK * 2), &tmB, bar,
+                        kb * BK, nb * bn + (int)rank * b_rows, MC_MASK);
           } else {
             // all TMA bytes of the pair land on the leader's barrier
             const uint32_t bar = CG == 2 ? mapa_rank(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
-            if (leader) mbar_expect_tx(&full[stage], CG * (C::A_BYTES + C::B_BYTES));
+            if (leader)
+              mbar_expect_tx(&full[stage], CG == 2 ? 2 * (C::A_BYTES + C::B_BYTES)
+                                                   : C::A_BYTES + bn * BK * 2);
             tma_load<CG>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
                          mb * C::TILE_M + (int)rank * 128);
             tma_load<CG>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
-                         nb * BN + (int)rank * C::B_ROWS);
+                         nb * bn + (int)rank * C::B_ROWS);
           }
         }
         __syncwarp();
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BN;   // accumulators 256 columns apart
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -376,10 +381,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const int64_t row0 = (int64_t)mb * C::TILE_M + rank * 128 + quad * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < bn / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
-        const int col0 = nb * BN + c * 32;
+        const int col0 = nb * bn + c * 32;
         if (col0 >= N) continue;
         uint8_t* buf = stg + (nchunk & 1) * STG_BUF;
         ++nchunk;
@@ -441,7 +446,7 @@ static int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, i
 
 template <typename T, int CG>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int64_t M,
-                  int N, int K, uint32_t idesc, const EpiParams& ep, cudaStream_t s) {
+                  int N, int K, uint32_t idesc, int bn, const EpiParams& ep, cudaStream_t s) {
   // L2 rasterisation: GROUP_M m-tiles share each weight (B) panel while it is
   // L2-resident (KRR_GEMM_GROUP_M overrides, fixed per process).
   static int group_m_env = -1, raster = -1;
@@ -459,7 +464,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   int group_m = group_m_env;
   {
     const double A = (double)M * K * 2, B = (double)N * K * 2;
-    const int num_m = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M), num_n = (N + BN - 1) / BN;
+    const int num_m = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M), num_n = (N + bn - 1) / bn;
     int gn = (int)((40.0 * (1 << 20)) / (256.0 * K * 2));      // ~40 MB weight band
     gn = std::max(1, std::min(gn, num_n));
     const double cost_m = A + B * std::max(1.0, (double)num_m / group_m_env);
@@ -472,7 +477,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
     cudaFuncSetAttribute(gemm_tcgen05_kernel<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
-  const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + BN - 1) / BN);
+  const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + bn - 1) / bn);
   constexpr int CS = cluster_size<CG>();
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(THREADS);
@@ -500,7 +505,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   }
   const int grid = std::min(CS * tiles, CS * max_clusters);
   cfg.gridDim = dim3(grid);
-  cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, CG>, ma, mb, mo, M, N, K, idesc, group_m, ep);
+  cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, CG>, ma, mb, mo, M, N, K, idesc, group_m, bn, ep);
   return check_launch(CG == 2 ? "gemm_tcgen05_2cta" : CG >= 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
 }
 
@@ -533,15 +538,32 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
     env_mode = e ? atoi(e) : 4;
     if (env_mode < 1 || env_mode > 5) env_mode = 4;
   }
-  const int mode = env_mode == 3 ? (K <= 4096 && M >= 1024 ? 2 : 1) : env_mode;
+  int mode = env_mode == 3 ? (K <= 4096 && M >= 1024 ? 2 : 1) : env_mode;
+  if (mode == 4 && M <= 128) mode = 1;   // one 128-row tile: a cluster partner would idle
   const CUtensorMapDataType dt =
       act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const int tile_m = mode == 2 ? 256 : 128;
+  // N-tile width (modes 1/4): 256, halved (to 64 at most) while the 128-row x
+  // bn tiles would not cover the SMs once — small batches (host-tier groups,
+  // the per-query latency path) are weight-streaming bound and need every SM
+  // pulling weights.  Every width runs the same per-element MMA sequence (full
+  // K in BK-chunk order into one fp32 accumulator), so the choice may depend
+  // on M without breaking batch invariance.  KRR_GEMM_NARROW=0 disables.
+  static int narrow = -1;
+  if (narrow < 0) {
+    const char* e = getenv("KRR_GEMM_NARROW");
+    narrow = e ? atoi(e) : 1;
+  }
+  int bn = BN;
+  if (narrow && (mode == 1 || mode == 4)) {
+    const int64_t num_m = (M + 127) / 128;
+    while (bn > 64 && num_m * ((N + bn - 1) / bn) < device_sm_count()) bn /= 2;
+  }
   CUtensorMap ma, mb, mo;
   int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK,
-                mode == 5 ? 64 : (mode == 2 || mode == 4) ? 128 : 256,
+                mode == 5 ? 64 : mode == 2 ? 128 : mode == 4 ? bn / 2 : bn,
                 CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   if (ep.kind == KRR_EPI_RESIDUAL) {
@@ -557,17 +579,17 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (rc) return rc;
   // instruction descriptor: D=f32 @4, A/B f16|bf16 @7/@10, K-major both, N>>3 @17, M>>4 @24
   const uint32_t fmt = act_dtype == KRR_BF16 ? 1u : 0u;
-  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
+  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(bn >> 3) << 17) |
                          ((uint32_t)(tile_m >> 4) << 24);
   if (act_dtype == KRR_F16)
-    return mode == 2   ? launch<__half, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
-           : mode == 4 ? launch<__half, 3>(ma, mb, mo, M, N, K, idesc, ep, s)
-           : mode == 5 ? launch<__half, 4>(ma, mb, mo, M, N, K, idesc, ep, s)
-                       : launch<__half, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
-  return mode == 2   ? launch<__nv_bfloat16, 2>(ma, mb, mo, M, N, K, idesc, ep, s)
-         : mode == 4 ? launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, ep, s)
-         : mode == 5 ? launch<__nv_bfloat16, 4>(ma, mb, mo, M, N, K, idesc, ep, s)
-                     : launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, ep, s);
+    return mode == 2   ? launch<__half, 2>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+           : mode == 4 ? launch<__half, 3>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+           : mode == 5 ? launch<__half, 4>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+                       : launch<__half, 1>(ma, mb, mo, M, N, K, idesc, bn, ep, s);
+  return mode == 2   ? launch<__nv_bfloat16, 2>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+         : mode == 4 ? launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+         : mode == 5 ? launch<__nv_bfloat16, 4>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+                     : launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, bn, ep, s);
 }
 
 }  // namespace krr

@@ -226,7 +226,8 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
     SSD/DRAM tier).
 
     Distinct documents are streamed H2D (cudaMemcpyAsync on ``copy_stream``)
-    into one half of a double-buffered HBM staging pool while the main stream
+    into one half of a double-buffered HBM staging pool (a quantised tier lands
+    codes and is dequantised on the main stream) while the main stream
     scores every pair of the previously landed half; events order the reuse of
     each half.  Each document crosses PCIe once per call however many pairs
     reference it.  Returns f32 [n] scores on the device (pair order)."""
@@ -252,16 +253,32 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
     cs = copy_stream or torch.cuda.Stream(device=dev)
     ready = [torch.cuda.Event() for _ in range(2)]
     free = [torch.cuda.Event() for _ in range(2)]
-    for gi, grp in enumerate(groups):
+
+    def slots_of(gi):
         b = gi & 1
-        slots = st_slots[b * half:b * half + grp.size]
+        return st_slots[b * half:b * half + groups[gi].size]
+
+    def issue_copy(gi):
+        b = gi & 1
         with torch.cuda.stream(cs):
             if gi >= 2:
                 cs.wait_event(free[b])
-            for h, s in zip(grp, slots):
-                tier.copy_in(int(h), staging, int(s), int(s))
+            for h, s in zip(groups[gi], slots_of(gi)):
+                tier.h2d(int(h), staging, int(s), int(s))
             ready[b].record(cs)
+
+    # both halves' transfers are queued before any scoring is, so the host
+    # thread enqueueing a group's layers never delays the next transfer
+    for gi in range(min(2, len(groups))):
+        issue_copy(gi)
+    for gi, grp in enumerate(groups):
+        b = gi & 1
+        slots = slots_of(gi)
         main.wait_event(ready[b])
+        # a quantised tier expands on the main stream, keeping the copy stream
+        # (and the PCIe link) busy with the next group's transfers
+        for s in slots:
+            tier.expand(staging, int(s), int(s))
         staging.set_valid_len(slots, tier.valid_len[grp])
         slot_of = dict(zip(grp.tolist(), slots.tolist()))
         sel = np.nonzero(np.isin(hs, grp))[0]
@@ -270,6 +287,8 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
                          q.index_select(0, sel_t), max_rows=max_rows)
         scores[sel_t] = sc
         free[b].record(main)
+        if gi + 2 < len(groups):
+            issue_copy(gi + 2)
     return scores
 
 

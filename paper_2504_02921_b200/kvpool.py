@@ -226,13 +226,26 @@ class HostKVTier:
         """Queue the H2D transfer of host page h into staging slot s on the
         current stream (plus the dequant kernel for a quantised tier; k picks
         the device landing buffer)."""
-        import torch
+        self.h2d(h, staging, s, k)
+        self.expand(staging, s, k)
+
+    def h2d(self, h: int, staging: KVPool, s: int, k: int = 0) -> None:
+        """The PCIe half of copy_in: page h -> staging slot s (16-bit tier) or
+        -> landing buffer k (quantised tier), on the current stream."""
         if self.quant is None:
             staging.slab[s].copy_(self.slab[h], non_blocking=True)
             return
         codes, scales = self._device_bufs(staging.device, staging.capacity)
         codes[k].copy_(self.codes[h], non_blocking=True)
         scales[k].copy_(self.scales[h], non_blocking=True)
+
+    def expand(self, staging: KVPool, s: int, k: int = 0) -> None:
+        """The HBM half of copy_in: dequantise landing buffer k into staging
+        slot s on the current stream (no-op for a 16-bit tier)."""
+        if self.quant is None:
+            return
+        import torch
+        codes, scales = self._device_bufs(staging.device, staging.capacity)
         KVH, D, HD = self.page_shape[2:]
         stream = torch.cuda.current_stream(staging.device).cuda_stream
         _lib.check(_lib.lib().krr_dequant_pages(

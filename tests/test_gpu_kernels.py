@@ -100,6 +100,22 @@ def test_gemm_batch_invariance_tcgen05():
     assert torch.equal(full[500:833], part)
 
 
+@pytest.mark.parametrize("epi", [_lib.EPI_STORE, _lib.EPI_GELU])
+def test_gemm_batch_invariance_across_tile_widths(epi):
+    """Small batches run narrower N tiles (and no cluster); the per-element MMA
+    sequence is unchanged, so a row's bits must not change with M."""
+    K, N, M = 1024, 1536, 20000            # full: 256-wide tiles; 96 / 700 rows: 64 / 128
+    A = (torch.randn(M, K, device="cuda") * 0.5).half()
+    B = (torch.randn(N, K, device="cuda") * 0.03).half()
+    full = torch.empty(M, N, dtype=torch.float16, device="cuda")
+    _gemm(_lib.GEMM_TCGEN05, _lib.F16, A, B, epi, full)
+    for r0, m in ((4096, 96), (777, 700), (0, 2500)):
+        part = torch.empty(m, N, dtype=torch.float16, device="cuda")
+        _gemm(_lib.GEMM_TCGEN05, _lib.F16, A[r0:r0 + m].contiguous(), B, epi, part)
+        torch.cuda.synchronize()
+        assert torch.equal(full[r0:r0 + m], part), (r0, m)
+
+
 def _rope_ref(x, pos, cos, sin):
     # x [..., HD] rotated as complex pairs (model.py:144,370-371)
     a, b = x[..., 0::2], x[..., 1::2]

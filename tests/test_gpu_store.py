@@ -193,12 +193,13 @@ def test_host_tier_streaming_matches_device_pool(model16):
 @pytest.mark.parametrize("bits,scheme", [(8, codec.QuantScheme.INT8_PER_CHANNEL),
                                          (4, codec.QuantScheme.INT4_PER_CHANNEL)])
 @pytest.mark.parametrize("src", ["f32", "f16"])
-def test_quant_pages_bit_exact_vs_host_codec(bits, scheme, src):
+@pytest.mark.parametrize("HD", [64, 40])               # 40: the scalar (non-vector) dequant
+def test_quant_pages_bit_exact_vs_host_codec(bits, scheme, src, HD):
     """krr_quant_pages / krr_dequant_pages == codec.quantize_tensor /
     dequantize_tensor (the reference's codec.py:58-95 semantics), tensor by tensor."""
     from paper_2504_02921_b200 import _lib
     rng = np.random.default_rng(bits)
-    n, KVH, D, HD = 4, 2, 37, 64                       # odd D*... exercises int4 packing
+    n, KVH, D = 4, 2, 37                                # odd D*... exercises int4 packing
     x = (rng.standard_normal((n, KVH, D, HD)) * 3).astype(np.float32)
     x[1, 0, :, 5] = 0.0                                 # all-zero channel -> scale 1
     x[2, 1, 3, 7] = 2.5                                 # exact .5 tie after scaling is likely
@@ -223,6 +224,12 @@ def test_quant_pages_bit_exact_vs_host_codec(bits, scheme, src):
         assert c_h[t * tb:(t + 1) * tb].tobytes() == q, t
         assert np.array_equal(s_h[t * KVH * HD:(t + 1) * KVH * HD].reshape(KVH, HD), sc), t
         assert np.array_equal(o_h[t], codec.dequantize_tensor(q, sc, scheme, (KVH, D, HD))), t
+    # 16-bit landing (the staging-pool path): the f32 product rounded once
+    o16 = torch.empty(n, KVH, D, HD, dtype=torch.float16, device="cuda")
+    _lib.check(_lib.lib().krr_dequant_pages(codes.data_ptr(), scales.data_ptr(), bits, n, KVH, D,
+                                            HD, _lib.F16, o16.data_ptr(), s))
+    torch.cuda.synchronize()
+    assert np.array_equal(o16.cpu().numpy(), o_h.astype(np.float16))
 
 
 @pytest.mark.parametrize("quant,scheme", [("int8", codec.QuantScheme.INT8_PER_CHANNEL),

@@ -42,6 +42,8 @@ def main():
     out = torch.empty(n * T, KVH * G * HD, dtype=torch.float16, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     kv_bytes = n * KVH * 2 * (P + T) * HD * es
+    # QK^T + PV over the visible keys (prefix + causal suffix)
+    flops = 4.0 * n * KVH * G * HD * (T * P + T * (T + 1) / 2)
     names = {"mma": _lib.ATTN_MMA, "tc": _lib.ATTN_TCGEN05}
     for boost in a.boost:
         q = (torch.randn(n * KVH, G * T, HD, device="cuda") * sc * boost).half()
@@ -64,6 +66,7 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.reps
             print(f"boost {boost:5.1f} {name:4s} {ms:8.3f} ms  KV {kv_bytes / ms / 1e6:7.0f} GB/s  "
+                  f"{flops / ms / 1e9:6.0f} TF/s  "
                   f"finite={bool(torch.isfinite(out).all())}", flush=True)
 
 

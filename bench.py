@@ -40,6 +40,9 @@ CONFIGS = {
     "c4": ("c3_mistral7b", 2500, 64, 100, 20),
     # host-DRAM tier: corpus docs live in pinned host memory, streamed per step
     "c5": ("c5_mistral7b_d2048", 48, 1, 48, 20),
+    # f4 architecture variant: C3's workload on the real Mistral-7B block
+    # (SwiGLU 14336, 1/sqrt(HD) softmax scale) -- outside reference parity
+    "c3r": ("c3_mistral7b_real", 1000, 64, 100, 20),
 }
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x20: "sync_boost", 0x40: "sw_thermal_slowdown",
@@ -50,7 +53,9 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
 def suffix_flops_per_pair(cfg, D, Q):
     """2*L*P_layer*Q + 4*L*H*HD*sum_{j=1..Q}(D+j)."""
     d, H, KVH, HD, L = cfg.model_dim, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.layers
-    p_layer = d * (H + 2 * KVH) * HD + H * HD * d + 8 * d * d
+    F = getattr(cfg, "ffn", 4 * d)
+    n_mlp = 3 if getattr(cfg, "mlp", "gelu") != "gelu" else 2   # gate+up+down vs up+down
+    p_layer = d * (H + 2 * KVH) * HD + H * HD * d + n_mlp * d * F
     return 2 * L * p_layer * Q + 4 * L * H * HD * sum(D + j for j in range(1, Q + 1))
 
 

@@ -55,8 +55,18 @@ enum {
   KRR_EPI_STORE = 0,     /* out[M,N] (act dtype) = C                         */
   KRR_EPI_GELU = 1,      /* out[M,N] (act dtype) = gelu_tanh(C)              */
   KRR_EPI_RESIDUAL = 2,  /* resid[M,N] (f32) += C                            */
-  KRR_EPI_QKV_ROPE = 3   /* RoPE(q,k) then scatter q / k / v (see krr_qkv_t)  */
+  KRR_EPI_QKV_ROPE = 3,  /* RoPE(q,k) then scatter q / k / v (see krr_qkv_t)  */
+  /* gated MLP (architecture variants): B's rows interleave
+   * 32-row blocks of the gate and up projections (block 2p = gate rows
+   * 32p..32p+31, block 2p+1 = up rows 32p..32p+31); N % 64 == 0 and
+   * out[M, N/2] (act dtype) = act(gate) * up                               */
+  KRR_EPI_GLU_GELU = 4,  /* GeGLU  (Gemma): gelu_tanh(gate) * up             */
+  KRR_EPI_GLU_SILU = 5   /* SwiGLU (Mistral/Llama): silu(gate) * up         */
 };
+
+/* MLP kinds (krr_model_t.mlp_kind) */
+enum { KRR_MLP_GELU = 0 /* reference: gelu_tanh(x W_up) W_down, 4d */,
+       KRR_MLP_GEGLU = 1, KRR_MLP_SWIGLU = 2 };
 
 /* GEMM backends */
 enum { KRR_GEMM_AUTO = 0, KRR_GEMM_TCGEN05 = 1, KRR_GEMM_SIMT = 2 };
@@ -92,8 +102,12 @@ typedef struct {
   const float* const* mlp_gain;
   const void* const* wqkv;        /* host array [L] of device [(H+2KVH)*HD, d] */
   const void* const* wo;          /* [d, H*HD] */
-  const void* const* w_up;        /* [4d, d]   */
-  const void* const* w_down;      /* [d, 4d]   */
+  const void* const* w_up;        /* [F, d] (gated kinds: [2F, d], gate/up 32-row interleave) */
+  const void* const* w_down;      /* [d, F]   */
+  /* architecture variants (zero-initialised = the reference model) */
+  int32_t ffn_dim;                /* F; 0 = 4d                                  */
+  int32_t mlp_kind;               /* KRR_MLP_*                                  */
+  float embed_scale;              /* x = E[tok] * scale (Gemma: sqrt(d)); 0 = 1 */
 } krr_model_t;
 
 /* A batch of sequences run through the layer stack together.  Every

@@ -124,10 +124,21 @@ class OracleConfig:
     seed: int = 0
     document_len: int = 256
     query_len: int = 48
+    # architecture variants (not in the reference -- defaults
+    # are the reference model): gated MLP kind and width, Gemma embedding
+    # scale, softmax scale on q.k
+    mlp: str = "gelu"
+    ffn_dim: int = 0
+    embed_scale: float = 1.0
+    attn_scale: float = 1.0
 
     @property
     def group(self) -> int:
         return self.heads // self.kv_heads
+
+    @property
+    def ffn(self) -> int:
+        return self.ffn_dim or 4 * self.model_dim
 
 
 @dataclass
@@ -136,14 +147,15 @@ class OracleWeights:
     emb: np.ndarray                 # [V, d] f32
     wqkv: list                      # per layer [d, (H+2KVH)HD]   (x @ W orientation)
     wo: list                        # per layer [H*HD, d]
-    w_up: list                      # per layer [d, 4d]
-    w_down: list                    # per layer [4d, d]
+    w_up: list                      # per layer [d, F]   (F = 4d for the reference)
+    w_down: list                    # per layer [F, d]
     attn_gain: list
     mlp_gain: list
     final_gain: np.ndarray
     cos: np.ndarray                 # [max_position, HD/2]
     sin: np.ndarray
     head: np.ndarray                # [d] score head
+    w_gate: list | None = None      # per layer [d, F] (gated-MLP variants only)
 
 
 def init_weights(cfg: OracleConfig, layers=None, with_embedding=True,
@@ -155,7 +167,8 @@ def init_weights(cfg: OracleConfig, layers=None, with_embedding=True,
     """
     d, h, kvh, hd = cfg.model_dim, cfg.heads, cfg.kv_heads, cfg.head_dim
     idx = range(cfg.layers) if layers is None else layers
-    wqkv, wo, up, down = ([None] * cfg.layers for _ in range(4))
+    wqkv, wo, up, down, gate = ([None] * cfg.layers for _ in range(5))
+    F = cfg.ffn
     for i in idx:
         p = f"layers.{i}"
         wqkv[i] = np.concatenate([init_tensor(cfg.seed, f"{p}.attn.wq", (d, h * hd)),
@@ -163,8 +176,10 @@ def init_weights(cfg: OracleConfig, layers=None, with_embedding=True,
                                   init_tensor(cfg.seed, f"{p}.attn.wv", (d, kvh * hd))],
                                  axis=1)
         wo[i] = init_tensor(cfg.seed, f"{p}.attn.wo", (h * hd, d))
-        up[i] = init_tensor(cfg.seed, f"{p}.mlp.w_up", (d, 4 * d))
-        down[i] = init_tensor(cfg.seed, f"{p}.mlp.w_down", (4 * d, d))
+        up[i] = init_tensor(cfg.seed, f"{p}.mlp.w_up", (d, F))
+        down[i] = init_tensor(cfg.seed, f"{p}.mlp.w_down", (F, d))
+        if cfg.mlp != "gelu":
+            gate[i] = init_tensor(cfg.seed, f"{p}.mlp.w_gate", (d, F))
     ones = [np.ones(d, np.float32) for _ in range(cfg.layers)]
     if lazy_embedding:
         emb = LazyEmbedding(cfg.seed, cfg.vocab_size, d)
@@ -173,7 +188,8 @@ def init_weights(cfg: OracleConfig, layers=None, with_embedding=True,
                if with_embedding else None)
     cos, sin = rope_tables(cfg.rope_base, hd, cfg.max_position)
     return OracleWeights(cfg, emb, wqkv, wo, up, down, ones, list(ones),
-                         np.ones(d, np.float32), cos, sin, score_head(cfg))
+                         np.ones(d, np.float32), cos, sin, score_head(cfg),
+                         gate if cfg.mlp != "gelu" else None)
 
 
 def round_weights(w: OracleWeights, dtype=np.float16) -> OracleWeights:
@@ -181,7 +197,8 @@ def round_weights(w: OracleWeights, dtype=np.float16) -> OracleWeights:
     multiplies with) so 16-bit parity compares activation rounding only."""
     r = lambda ms: [None if m is None else m.astype(dtype).astype(np.float32) for m in ms]
     return OracleWeights(w.cfg, w.emb, r(w.wqkv), r(w.wo), r(w.w_up), r(w.w_down),
-                         w.attn_gain, w.mlp_gain, w.final_gain, w.cos, w.sin, w.head)
+                         w.attn_gain, w.mlp_gain, w.final_gain, w.cos, w.sin, w.head,
+                         None if w.w_gate is None else r(w.w_gate))
 
 
 # --------------------------------------------------------------------------
@@ -196,6 +213,18 @@ def _rms(x: np.ndarray, gain: np.ndarray) -> np.ndarray:
 def _gelu(x: np.ndarray) -> np.ndarray:
     """tanh GELU (model.py:444-446)."""
     return np.float32(0.5) * x * (np.float32(1.0) + np.tanh(_GELU_A * (x + _GELU_B * x * x * x)))
+
+
+def _mlp(w: OracleWeights, li: int, xn: np.ndarray) -> np.ndarray:
+    """Reference MLP gelu(xn W_up) W_down (model.py:399-400); the gated
+    variants (f4) use act(xn W_gate) * (xn W_up) with act = gelu (GeGLU) or
+    silu (SwiGLU), as in Gemma / Mistral."""
+    kind = w.cfg.mlp
+    if kind == "gelu":
+        return _gelu(xn @ w.w_up[li]) @ w.w_down[li]
+    g = xn @ w.w_gate[li]
+    act = _gelu(g) if kind == "geglu" else g / (np.float32(1.0) + np.exp(-g))
+    return (act * (xn @ w.w_up[li])) @ w.w_down[li]
 
 
 def _rotate(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
@@ -239,6 +268,8 @@ def forward(w: OracleWeights, tokens, positions, past_k=None, past_v=None, valid
     bias = np.where(vis, np.float32(0.0), np.float32(-np.inf))
 
     x = np.asarray(w.emb[tokens], np.float32) if x_in is None else x_in.astype(np.float32)
+    if x_in is None and cfg.embed_scale != 1.0:
+        x = x * np.float32(cfg.embed_scale)
     new_k = np.zeros((L, KVH, T, HD), np.float32)
     new_v = np.zeros_like(new_k)
     layers = range(L) if layer_range is None else layer_range
@@ -247,7 +278,10 @@ def forward(w: OracleWeights, tokens, positions, past_k=None, past_v=None, valid
             capture[li] = x.copy()
         xn = _rms(x, w.attn_gain[li])
         qkv = xn @ w.wqkv[li]
-        q = _rotate(qkv[:, :H * HD].reshape(T, H, HD), cos, sin)
+        qp = qkv[:, :H * HD]
+        if cfg.attn_scale != 1.0:                        # variant: scaled q.k
+            qp = qp * np.float32(cfg.attn_scale)
+        q = _rotate(qp.reshape(T, H, HD), cos, sin)
         k = _rotate(qkv[:, H * HD:(H + KVH) * HD].reshape(T, KVH, HD), cos, sin)
         v = qkv[:, (H + KVH) * HD:].reshape(T, KVH, HD)
         new_k[li] = k.transpose(1, 0, 2)
@@ -269,7 +303,7 @@ def forward(w: OracleWeights, tokens, positions, past_k=None, past_v=None, valid
             o = np.einsum("gtj,jc->gtc", e, vals) / z              # (P V)/z, model.py:391-394
             out[:, kh * G:(kh + 1) * G, :] = o.transpose(1, 0, 2)
         x = x + out.reshape(T, H * HD) @ w.wo[li]                  # model.py:395-397
-        x = x + _gelu(_rms(x, w.mlp_gain[li]) @ w.w_up[li]) @ w.w_down[li]  # model.py:399-400
+        x = x + _mlp(w, li, _rms(x, w.mlp_gain[li]))                # model.py:399-400
     return (x if return_residual else _rms(x, w.final_gain)), new_k, new_v
 
 

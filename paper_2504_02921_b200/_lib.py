@@ -17,7 +17,8 @@ LIB_PATH = os.environ.get("KRR_LIB") or os.path.join(os.path.dirname(os.path.abs
 
 F32, F16, BF16 = 0, 1, 2
 DTYPE_CODES = {"f32": F32, "f16": F16, "bf16": BF16}
-EPI_STORE, EPI_GELU, EPI_RESIDUAL, EPI_QKV_ROPE = 0, 1, 2, 3
+EPI_STORE, EPI_GELU, EPI_RESIDUAL, EPI_QKV_ROPE, EPI_GLU_GELU, EPI_GLU_SILU = 0, 1, 2, 3, 4, 5
+MLP_GELU, MLP_GEGLU, MLP_SWIGLU = 0, 1, 2
 GEMM_AUTO, GEMM_TCGEN05, GEMM_SIMT = 0, 1, 2
 ATTN_AUTO, ATTN_MMA, ATTN_SIMT, ATTN_TCGEN05 = 0, 1, 2, 3
 ATTN_TC = ATTN_MMA
@@ -46,7 +47,8 @@ class Model(C.Structure):
                 ("act_dtype", i32), ("gemm_backend", i32), ("attn_backend", i32),
                 ("token_embedding", vp), ("rope_cos", vp), ("rope_sin", vp),
                 ("final_gain", vp), ("score_head", vp), ("attn_gain", vp), ("mlp_gain", vp),
-                ("wqkv", vp), ("wo", vp), ("w_up", vp), ("w_down", vp)]
+                ("wqkv", vp), ("wo", vp), ("w_up", vp), ("w_down", vp),
+                ("ffn_dim", i32), ("mlp_kind", i32), ("embed_scale", C.c_float)]
 
 
 class Batch(C.Structure):

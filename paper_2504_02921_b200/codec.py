@@ -31,15 +31,21 @@ HEADER = struct.Struct("<4sHB6H")      # codec.py:29-31
 
 
 class QuantScheme(enum.Enum):
-    """Scheme codes 0/2/3 as in codec.py:34-56 (code 1 is unused there)."""
+    """Scheme codes 0/2/3 as in codec.py:34-56.  Code 1 is unused by the
+    reference; this build assigns it to F16 (IEEE binary16 payload, the HBM
+    pool's own page format, half the bytes of F32, no scales).  The reference
+    decoder rejects code 1 (codec.py:170-173), so F16 entries are for stores
+    this build reads; export F32/INT8/INT4 for reference interop."""
 
     F32 = 0
+    F16 = 1
     INT8_PER_CHANNEL = 2
     INT4_PER_CHANNEL = 3
 
     @classmethod
     def from_name(cls, name: str) -> "QuantScheme":
-        table = {"F32": cls.F32, "FLOAT32": cls.F32, "INT8": cls.INT8_PER_CHANNEL,
+        table = {"F32": cls.F32, "FLOAT32": cls.F32, "F16": cls.F16, "FLOAT16": cls.F16,
+                 "HALF": cls.F16, "INT8": cls.INT8_PER_CHANNEL,
                  "KV8": cls.INT8_PER_CHANNEL, "INT4": cls.INT4_PER_CHANNEL,
                  "KV4": cls.INT4_PER_CHANNEL}
         try:
@@ -49,11 +55,15 @@ class QuantScheme(enum.Enum):
 
     @property
     def short_name(self) -> str:
-        return {0: "f32", 2: "int8", 3: "int4"}[self.value]
+        return {0: "f32", 1: "f16", 2: "int8", 3: "int4"}[self.value]
 
     @property
     def bits(self) -> int:
-        return {0: 32, 2: 8, 3: 4}[self.value]
+        return {0: 32, 1: 16, 2: 8, 3: 4}[self.value]
+
+    @property
+    def quantised(self) -> bool:
+        return self.value >= 2
 
     @property
     def level(self) -> int:
@@ -64,7 +74,7 @@ def payload_nbytes(layers: int, kv_heads: int, document_len: int, head_dim: int,
                    scheme: QuantScheme) -> int:
     """Payload bytes of one entry, header and scales excluded (codec.py:118-125)."""
     n = kv_heads * document_len * head_dim
-    per = {32: 4 * n, 8: n, 4: (n + 1) // 2}[scheme.bits]
+    per = {32: 4 * n, 16: 2 * n, 8: n, 4: (n + 1) // 2}[scheme.bits]
     return 2 * layers * per
 
 
@@ -74,8 +84,8 @@ def quantize_tensor(t: np.ndarray, scheme: QuantScheme) -> tuple[bytes, np.ndarr
     f32 tensor (codec.py:58-79): scale = amax/level (1.0 for an all-zero
     channel), code = clamp(round-half-away(t/scale), +-level); INT4 packs two
     codes per byte, low nibble first."""
-    if scheme is QuantScheme.F32:
-        raise CodecError("F32 stores raw floats; nothing to quantize")
+    if not scheme.quantised:
+        raise CodecError(f"{scheme.name} stores raw floats; nothing to quantize")
     t = np.asarray(t, np.float32)
     if t.ndim != 3:
         raise CodecError("expected a [heads, tokens, channels] tensor")
@@ -118,7 +128,7 @@ def dequantize_tensor(qdata: bytes, scales: np.ndarray, scheme: QuantScheme,
             raise CodecError(f"int8 payload has {len(qdata)} bytes, expected {count}")
         codes = np.frombuffer(qdata, np.int8)
     else:
-        raise CodecError("F32 stores raw floats; nothing to dequantize")
+        raise CodecError(f"{scheme.name} stores raw floats; nothing to dequantize")
     return codes.reshape(shape).astype(np.float32) * np.asarray(scales, np.float32)[:, None, :]
 
 
@@ -166,7 +176,7 @@ def parse_entry(data) -> EntryView:
     v.chunk_id = bytes(data[off:off + idn]).decode("utf-8")
     off += idn
     n_t = 2 * L
-    scale_bytes = 0 if scheme is QuantScheme.F32 else KVH * HD * 4
+    scale_bytes = KVH * HD * 4 if scheme.quantised else 0
     v.tensor_bytes = payload_nbytes(1, KVH, D, HD, scheme) // 2
     v.scales_off = off
     v.payload_off = off + n_t * scale_bytes
@@ -193,6 +203,13 @@ def encode_arrays(chunk_id: str, keys: np.ndarray, values: np.ndarray, valid_len
     if scheme is QuantScheme.F32:
         kv = np.stack([np.asarray(keys, "<f4"), np.asarray(values, "<f4")], axis=1)
         return b"".join(head) + np.ascontiguousarray(kv).tobytes()
+    if scheme is QuantScheme.F16:
+        kv = np.stack([np.asarray(keys, np.float32), np.asarray(values, np.float32)], axis=1)
+        with np.errstate(over="ignore"):
+            h = kv.astype("<f2")                          # round to nearest even
+        if not np.isfinite(h).all():
+            raise CodecError("KV element outside the f16 range")
+        return b"".join(head) + np.ascontiguousarray(h).tobytes()
     scales, payload = [], []
     for li in range(L):
         for t in (keys[li], values[li]):
@@ -211,6 +228,25 @@ def encode_entry(doc_kv, scheme: QuantScheme = QuantScheme.F32) -> bytes:
     return encode_arrays(doc_kv.chunk_id, kv.keys, kv.values, doc_kv.valid_len, scheme)
 
 
+def encode_pool_page(chunk_id: str, pool, slot: int,
+                     scheme: QuantScheme = QuantScheme.F32) -> bytes:
+    """Serialise an HBM pool page.  F16 from an f16 pool is the page's own
+    bytes behind the header (one D2H copy, no f32 round trip); other schemes
+    go through f32 arrays as encode_arrays."""
+    import torch
+    if scheme is QuantScheme.F16 and pool.slab.dtype == torch.float16:
+        L, _, KVH, D, HD = pool.page_shape
+        cid = chunk_id.encode("utf-8")
+        head = HEADER.pack(MAGIC, VERSION, scheme.value, L, KVH, D, HD,
+                           pool.host_valid_len(slot), len(cid))
+        page = pool.slab[slot].cpu().numpy()
+        if not np.isfinite(page).all():
+            raise CodecError("non-finite element in KV page")
+        return head + cid + page.tobytes()
+    k, v = pool.read_host_kv(slot)
+    return encode_arrays(chunk_id, k, v, pool.host_valid_len(slot), scheme)
+
+
 def decode_arrays(data):
     """(chunk_id, keys, values, valid_len) as f32; F32 entries give read-only
     views over ``data`` (codec.py:190-195)."""
@@ -220,6 +256,11 @@ def decode_arrays(data):
         arr = np.frombuffer(data, "<f4", 2 * L * KVH * D * HD, v.payload_off)
         arr = arr.reshape(L, 2, KVH, D, HD)
         return v.chunk_id, arr[:, 0], arr[:, 1], v.valid_len
+    if v.scheme is QuantScheme.F16:
+        arr = np.frombuffer(data, "<f2", 2 * L * KVH * D * HD, v.payload_off)
+        arr = arr.reshape(L, 2, KVH, D, HD).astype(np.float32)
+        return v.chunk_id, np.ascontiguousarray(arr[:, 0]), np.ascontiguousarray(arr[:, 1]), \
+            v.valid_len
     sc = v.scales()
     keys = np.empty((L, KVH, D, HD), np.float32)
     values = np.empty_like(keys)
@@ -243,8 +284,8 @@ def decode_entry(data):
 def decode_entry_to_pool(data, pool, slot: int | None = None, stream=None):
     """Decode an entry straight into an HBM pool page; returns the DocKV handle.
 
-    F32: the payload bytes are copied H2D once and cast to the pool dtype on
-    the GPU.  INT8/INT4: codes + scales are copied H2D and expanded by the
+    F32 / F16: the payload bytes are copied H2D once and cast to the pool
+    dtype on the GPU (F16 into an f16 pool is a plain copy).  INT8/INT4: codes + scales are copied H2D and expanded by the
     krr_dequant_kv kernel, one launch per (layer, K|V) page."""
     import torch
 
@@ -261,8 +302,9 @@ def decode_entry_to_pool(data, pool, slot: int | None = None, stream=None):
     page = pool.slab[slot]
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     with torch.cuda.stream(st):
-        if v.scheme is QuantScheme.F32:
-            src = torch.frombuffer(bytearray(v.payload()), dtype=torch.float32)
+        if not v.scheme.quantised:
+            dt = torch.float32 if v.scheme is QuantScheme.F32 else torch.float16
+            src = torch.frombuffer(bytearray(v.payload()), dtype=dt)
             page.copy_(src.to(dev, non_blocking=False).view(page.shape))
         else:
             codes = torch.frombuffer(bytearray(v.payload()), dtype=torch.uint8).to(dev)

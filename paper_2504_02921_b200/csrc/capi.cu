@@ -87,11 +87,32 @@ __global__ void init_uniform_kernel(uint64_t seed, double bound, int64_t rows, i
 
 // a5: x = E[tokens]  (model.py:352)
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const float* __restrict__ emb,
-                             int d, float* __restrict__ x) {
+                             int d, float scale, float* __restrict__ x) {
   const int64_t r = blockIdx.x;
   const float4* src = reinterpret_cast<const float4*>(emb + (int64_t)tok[r] * d);
   float4* dst = reinterpret_cast<float4*>(x + r * d);
-  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+  if (scale == 1.0f) {
+    for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+  } else {   // Gemma-style embedding scale (architecture variant)
+    for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+      const float4 v = src[i];
+      dst[i] = make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale);
+    }
+  }
+}
+
+static int launch_embed(const int32_t* tokens, const float* emb, int64_t rows, int32_t d,
+                        float scale, float* x, cudaStream_t s) {
+  KRR_REQUIRE(d % 4 == 0, KRR_ESHAPE, "model_dim must be a multiple of 4");
+  if (rows == 0) return KRR_OK;
+  ProfScope ps(s, 2);
+  embed_kernel<<<(unsigned)rows, 128, 0, s>>>(tokens, emb, d, scale, x);
+  return check_launch("embed");
+}
+
+// F (MLP width) and the up-projection's GEMM width / epilogue for a model
+static inline int ffn_of(const krr_model_t* m) {
+  return m->ffn_dim > 0 ? m->ffn_dim : 4 * m->model_dim;
 }
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -370,7 +391,8 @@ static int do_gemm(int backend, int act, const void* A, const void* B, int64_t M
     // (K % 64, N % 32, 16-byte aligned operands); CUDA-core kernel otherwise
     // (e.g. the reference's default desk config, d=128 with 16-wide heads, is
     // fine; odd widths are not)
-    const bool tc_ok = act != KRR_F32 && K % 64 == 0 && N % 32 == 0 &&
+    const bool glu = ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU;
+    const bool tc_ok = act != KRR_F32 && K % 64 == 0 && N % (glu ? 64 : 32) == 0 &&
                        (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(B) & 15) == 0;
     backend = tc_ok ? KRR_GEMM_TCGEN05 : KRR_GEMM_SIMT;
@@ -491,11 +513,7 @@ int krr_init_uniform(uint64_t seed, double bound, int64_t rows, int64_t cols, in
 
 int krr_embed(const int32_t* tokens, const float* emb, int64_t rows, int32_t d, float* x,
               krr_stream_t stream) {
-  KRR_REQUIRE(d % 4 == 0, KRR_ESHAPE, "model_dim must be a multiple of 4");
-  if (rows == 0) return KRR_OK;
-  ProfScope ps((cudaStream_t)stream, 2);
-  embed_kernel<<<(unsigned)rows, 128, 0, (cudaStream_t)stream>>>(tokens, emb, d, x);
-  return check_launch("embed");
+  return launch_embed(tokens, emb, rows, d, 1.0f, x, (cudaStream_t)stream);
 }
 
 int krr_rmsnorm(const float* x, const float* gain, int64_t rows, int32_t d, int out_dtype,
@@ -509,7 +527,8 @@ int krr_gemm(int backend, int act_dtype, const void* A, const void* B, int64_t M
   EpiParams ep{};
   ep.kind = epilogue;
   ep.M = M;
-  ep.N = N;
+  // gated epilogues write N/2 columns (act(gate) * up)
+  ep.N = (epilogue == KRR_EPI_GLU_GELU || epilogue == KRR_EPI_GLU_SILU) ? N / 2 : N;
   ep.out = out;
   if (epilogue == KRR_EPI_QKV_ROPE) {
     KRR_REQUIRE(qkv != nullptr, KRR_ECONFIG, "QKV epilogue needs krr_qkv_t");
@@ -643,7 +662,7 @@ int krr_workspace_bytes(const krr_model_t* m, int64_t rows, size_t* out) {
                + align256(rows * d * es)         // xn (normed activations)
                + align256(rows * hq * es)        // q  ([unit][g*t][hd])
                + align256(rows * hq * es)        // attention output
-               + align256(rows * 4 * d * es);    // MLP hidden
+               + align256(rows * (int64_t)ffn_of(m) * es);    // MLP hidden
   *out = total;
   return KRR_OK;
 }
@@ -654,7 +673,13 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
   cudaStream_t s = (cudaStream_t)stream;
   const int L = m->layers, d = m->model_dim, H = m->heads, KVH = m->kv_heads, HD = m->head_dim;
   KRR_REQUIRE(H % KVH == 0 && H * HD == d, KRR_ECONFIG, "inconsistent model geometry");
+  KRR_REQUIRE(m->mlp_kind >= KRR_MLP_GELU && m->mlp_kind <= KRR_MLP_SWIGLU, KRR_ECONFIG,
+              "unknown mlp_kind");
   const int G = H / KVH;
+  const int F = ffn_of(m);
+  const bool gated = m->mlp_kind != KRR_MLP_GELU;
+  KRR_REQUIRE(!gated || F % 32 == 0, KRR_ECONFIG, "gated MLP needs ffn_dim % 32 == 0");
+  const int n_up = gated ? 2 * F : F;                 // up-projection GEMM width
   const int64_t rows = (int64_t)b->n_seqs * b->seq_len;
   if (rows == 0) return KRR_OK;
   KRR_REQUIRE(b->pos0 + b->seq_len <= m->max_position, KRR_ESHAPE, "positions exceed max_position");
@@ -678,14 +703,16 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
         cudaSuccess)
       return fail(KRR_ECUDA, "x_in copy failed");
   } else {
-    rc = krr_embed(b->tokens, m->token_embedding, rows, d, x, stream);
+    rc = launch_embed(b->tokens, m->token_embedding, rows, d,
+                      m->embed_scale > 0.f ? m->embed_scale : 1.0f, x, s);
     if (rc) return rc;
   }
   const int nqkv = (H + 2 * KVH) * HD;
   const bool prefill_only = b->scores == nullptr && b->x_out == nullptr;
   // last-layer row pruning needs the compact buffers to fit the dead regions
   const bool scoring_tail = b->scores != nullptr && b->x_out == nullptr &&
-                            b->last_index != nullptr && b->seq_len >= 4;
+                            b->last_index != nullptr && b->seq_len >= 4 &&
+                            (int64_t)b->seq_len * H * HD >= F;
   for (int l = 0; l < L; ++l) {
     rc = do_rmsnorm(x, m->attn_gain[l], rows, d, act, xn, s);
     if (rc) return rc;
@@ -710,8 +737,9 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     er.kind = KRR_EPI_RESIDUAL;
     er.out = x;
     EpiParams eg{};
-    eg.kind = KRR_EPI_GELU;
-    eg.N = 4 * d;
+    eg.kind = !gated ? KRR_EPI_GELU
+              : m->mlp_kind == KRR_MLP_GEGLU ? KRR_EPI_GLU_GELU : KRR_EPI_GLU_SILU;
+    eg.N = F;   // output width (the hidden); the GEMM itself is n_up wide
     if (scoring_tail && l == L - 1) {
       // Only the scored row of each sequence reaches the score head
       // (reranker.py:211-212): run this layer's WO + MLP on n rows.  Compact
@@ -720,7 +748,7 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
       void* ab_c = qb;                                      // [n, H*HD] act
       float* x_c = reinterpret_cast<float*>(xn);            // [n, d] f32
       void* xn_c = hb;                                      // [n, d] act
-      void* hb_c = ab;                                      // [n, 4d] act
+      void* hb_c = ab;                                      // [n, F] act
       {
         ProfScope ps(s, 2);
         if (es == 2)
@@ -740,9 +768,9 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
       rc = do_rmsnorm(x_c, m->mlp_gain[l], n, d, act, xn_c, s);
       if (rc) return rc;
       eg.M = n; eg.out = hb_c;
-      rc = do_gemm(m->gemm_backend, act, xn_c, m->w_up[l], n, 4 * d, d, eg, s);
+      rc = do_gemm(m->gemm_backend, act, xn_c, m->w_up[l], n, n_up, d, eg, s);
       if (rc) return rc;
-      rc = do_gemm(m->gemm_backend, act, hb_c, m->w_down[l], n, d, 4 * d, er, s);
+      rc = do_gemm(m->gemm_backend, act, hb_c, m->w_down[l], n, d, F, er, s);
       if (rc) return rc;
       return krr_score_head(x_c, b->n_seqs, 1, d, nullptr, m->final_gain, m->score_head,
                             b->scores, stream);
@@ -755,9 +783,9 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     if (rc) return rc;
     eg.M = rows;
     eg.out = hb;
-    rc = do_gemm(m->gemm_backend, act, xn, m->w_up[l], rows, 4 * d, d, eg, s);
+    rc = do_gemm(m->gemm_backend, act, xn, m->w_up[l], rows, n_up, d, eg, s);
     if (rc) return rc;
-    rc = do_gemm(m->gemm_backend, act, hb, m->w_down[l], rows, d, 4 * d, er, s);
+    rc = do_gemm(m->gemm_backend, act, hb, m->w_down[l], rows, d, F, er, s);
     if (rc) return rc;
   }
   if (b->x_out &&

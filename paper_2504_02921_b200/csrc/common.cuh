@@ -55,6 +55,9 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return 0.5f * x * (1.0f + tanhf(inner));
 }
 
+// SiLU for the SwiGLU variant: x * sigmoid(x)
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -51,7 +51,8 @@ __device__ __forceinline__ void epi_apply(const EpiParams& ep, int64_t row, int 
     }
     return;
   }
-  if (ep.kind == KRR_EPI_STORE || ep.kind == KRR_EPI_GELU) {
+  if (ep.kind == KRR_EPI_STORE || ep.kind == KRR_EPI_GELU || ep.kind == KRR_EPI_GLU_GELU ||
+      ep.kind == KRR_EPI_GLU_SILU) {   // GLU: v already holds act(gate) * up
     T* o = reinterpret_cast<T*>(ep.out) + row * (int64_t)ep.N + col0;
     const bool g = ep.kind == KRR_EPI_GELU;
 #pragma unroll 4

@@ -44,6 +44,34 @@ __global__ void __launch_bounds__(THREADS)
     }
     __syncthreads();
   }
+  if (ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU) {
+    // the 64-column tile is one (gate 32 | up 32) block pair: gate threads
+    // (tx < 8) publish act(gate) through shared memory, up threads combine
+    __shared__ float sG[TM][33];
+    const bool gelu = ep.kind == KRR_EPI_GLU_GELU;
+    if (tx < 8) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float g = acc[i][j];
+          sG[ty * 4 + i][tx * 4 + j] = gelu ? gelu_tanh(g) : g / (1.0f + expf(-g));
+        }
+    }
+    __syncthreads();
+    if (tx >= 8) {
+      const int oc = n0 / 2 + (tx - 8) * 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t row = m0 + ty * 4 + i;
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = sG[ty * 4 + i][(tx - 8) * 4 + j] * acc[i][j];
+        if (row < M) epi_apply<T>(ep, row, oc, v, 4);
+      }
+    }
+    return;
+  }
   const int col0 = n0 + tx * 4;
   if (col0 >= N) return;
 #pragma unroll
@@ -59,6 +87,8 @@ int launch_gemm_simt(int act_dtype, const void* A, const void* B, int64_t M, int
                      const EpiParams& ep, cudaStream_t s) {
   using namespace simt;
   KRR_REQUIRE(N % 2 == 0, KRR_ESHAPE, "SIMT GEMM needs even N");
+  KRR_REQUIRE((ep.kind != KRR_EPI_GLU_GELU && ep.kind != KRR_EPI_GLU_SILU) || N % 64 == 0,
+              KRR_ESHAPE, "gated-MLP GEMM needs N % 64 == 0");
   KRR_REQUIRE((M + TM - 1) / TM < 65535, KRR_ESHAPE, "SIMT GEMM: M too large for one launch");
   dim3 grid((N + TN - 1) / TN, (unsigned)((M + TM - 1) / TM));
   if (act_dtype == KRR_F32)

@@ -368,6 +368,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tempty0 =
         CG == 2 ? mapa_rank(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     int it = 0, nchunk = 0;
+    const bool glu = ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU;
+    float gate[32];
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       int mb, nb;
       tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
@@ -384,8 +386,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int c = 0; c < bn / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
-        const int col0 = nb * bn + c * 32;
+        int col0 = nb * bn + c * 32;
         if (col0 >= N) continue;
+        if (glu) {
+          // even chunk: gate (kept as act(gate)); odd chunk: up -> act(gate) * up
+          if (!(c & 1)) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float g = __uint_as_float(r[j]);
+              gate[j] = ep.kind == KRR_EPI_GLU_GELU ? gelu_fast(g) : silu(g);
+            }
+            continue;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(gate[j] * __uint_as_float(r[j]));
+          col0 = (col0 - 32) / 2;
+        }
         uint8_t* buf = stg + (nchunk & 1) * STG_BUF;
         ++nchunk;
         // the bulk op that last read this buffer (two chunks ago) must be done
@@ -570,9 +586,13 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
     KRR_REQUIRE((reinterpret_cast<uintptr_t>(ep.out) & 15) == 0, KRR_ESHAPE, "residual must be 16-byte aligned");
     rc = make_map(&mo, ep.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)N, (uint64_t)M, 32, 32,
                   CU_TENSOR_MAP_SWIZZLE_128B);
-  } else if (ep.kind == KRR_EPI_STORE || ep.kind == KRR_EPI_GELU) {
+  } else if (ep.kind == KRR_EPI_STORE || ep.kind == KRR_EPI_GELU || ep.kind == KRR_EPI_GLU_GELU ||
+             ep.kind == KRR_EPI_GLU_SILU) {
     KRR_REQUIRE((reinterpret_cast<uintptr_t>(ep.out) & 15) == 0, KRR_ESHAPE, "output must be 16-byte aligned");
-    rc = make_map(&mo, ep.out, dt, 2, (uint64_t)N, (uint64_t)M, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    const bool glu = ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU;
+    KRR_REQUIRE(!glu || N % 64 == 0, KRR_ESHAPE, "gated-MLP GEMM needs N % 64 == 0");
+    rc = make_map(&mo, ep.out, dt, 2, (uint64_t)(glu ? N / 2 : N), (uint64_t)M, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_64B);
   } else {
     mo = ma;  // unused by the QKV scatter
   }

@@ -306,7 +306,7 @@ def layer_slice(w: DeviceWeights, l0: int, l1: int):
     m = _lib.Model(l1 - l0, cfg.model_dim, cfg.heads, cfg.kv_heads, cfg.head_dim,
                    cfg.vocab_size, cfg.max_position, w.code, w.gemm_backend, w.attn_backend,
                    base.token_embedding, base.rope_cos, base.rope_sin, base.final_gain,
-                   base.score_head, *[C.cast(a, C.c_void_p) for a in keep])
+                   base.score_head, *[C.cast(a, C.c_void_p) for a in keep], *w.variant_fields())
     m._keep = keep
     return m
 

@@ -123,7 +123,7 @@ def populate_store(model: RerankModel, docs, index, store, scheme=None, path: st
     ``index`` anything with ``centroid_of(doc_id)`` (IvfIndex), ``store`` a
     ShardedStore.  Prefill runs batched on the GPU straight into pool pages.
     A shard backed by a DevicePagedKVStore keeps the page where the prefill
-    wrote it when the scheme is F32 (no bytes cross PCIe; the count is the
+    wrote it when the scheme is F32 or F16 (no bytes cross PCIe; the count is the
     entry size the reference would have written); other backends, and
     quantised schemes, receive HRKV bytes."""
     from .codec import HEADER, QuantScheme, encode_entry, payload_nbytes
@@ -142,7 +142,7 @@ def populate_store(model: RerankModel, docs, index, store, scheme=None, path: st
         for j, b in enumerate(targets):
             # quantised schemes go through the bytes (the page must hold the
             # dequantised values the reference would score with)
-            device = isinstance(b, DevicePagedKVStore) and scheme is QuantScheme.F32
+            device = isinstance(b, DevicePagedKVStore) and not scheme.quantised
             key = id(b.pool) if device else 0
             by_pool.setdefault(key, []).append(j)
         for key, js in by_pool.items():

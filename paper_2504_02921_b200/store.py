@@ -188,10 +188,14 @@ class DevicePagedKVStore(_Counted):
     ``host_tier`` attached, entries evicted from HBM (``spill``) stay
     addressable and are streamed back by ``ensure_resident``."""
 
-    def __init__(self, pool, host_tier=None):
+    def __init__(self, pool, host_tier=None, export_scheme=None):
+        from .codec import QuantScheme
         super().__init__()
         self.pool = pool
         self.host_tier = host_tier
+        # scheme of the bytes get() returns: F32 (reference-readable, default)
+        # or F16 (the page's own bytes, half the size; this build only)
+        self.export_scheme = export_scheme if export_scheme is not None else QuantScheme.F32
         self._entry_bytes: dict[str, int] = {}
 
     # -- reference duck type
@@ -206,13 +210,12 @@ class DevicePagedKVStore(_Counted):
             self._entry_bytes[key] = len(value)
 
     def get(self, key: str):
-        from .codec import encode_arrays
+        from .codec import encode_pool_page
         slot = int(self.pool.lookup([key])[0])
         if slot < 0:
             self._count_get(None)
             return None
-        k, v = self.pool.read_host_kv(slot)
-        data = encode_arrays(key, k, v, self.pool.host_valid_len(slot))
+        data = encode_pool_page(key, self.pool, slot, self.export_scheme)
         self._count_get(data)
         return data
 

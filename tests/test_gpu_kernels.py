@@ -76,6 +76,27 @@ def test_gemm_store_gelu_residual(backend, M, N, K):
     assert (x - (x0 + ref)).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
 
 
+@pytest.mark.parametrize("backend", [_lib.GEMM_TCGEN05, _lib.GEMM_SIMT])
+@pytest.mark.parametrize("epi", [_lib.EPI_GLU_GELU, _lib.EPI_GLU_SILU])
+@pytest.mark.parametrize("M,F,K", [(300, 256, 256), (77, 96, 128), (2048, 1024, 512)])
+def test_gemm_gated_mlp_epilogue(backend, epi, M, F, K):
+    """Gated-MLP epilogue (f4 variants): B interleaves 32-row gate / up blocks;
+    out[M, F] = act(A Wg^T) * (A Wu^T), act = tanh-GELU or SiLU."""
+    A = (torch.randn(M, K, device="cuda") * 0.5).half()
+    Wg = (torch.randn(F, K, device="cuda") * (1.0 / math.sqrt(K))).half()
+    Wu = (torch.randn(F, K, device="cuda") * (1.0 / math.sqrt(K))).half()
+    B = torch.stack([Wg.view(F // 32, 32, K), Wu.view(F // 32, 32, K)], 1).reshape(2 * F, K)
+    g, u = A.float() @ Wg.float().T, A.float() @ Wu.float().T
+    act = (torch.nn.functional.gelu(g, approximate="tanh") if epi == _lib.EPI_GLU_GELU
+           else torch.nn.functional.silu(g))
+    ref = act * u
+    out = torch.empty(M, F, dtype=torch.float16, device="cuda")
+    _gemm(backend, _lib.F16, A, B.contiguous(), epi, out)
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 4e-3 * max(1.0, ref.abs().max().item()), err
+
+
 def test_gemm_f32_simt_exact_order():
     M, N, K = 200, 128, 96
     A = torch.randn(M, K, device="cuda")

@@ -251,6 +251,50 @@ def test_other_configs_vs_oracle(cfg, lay, precision):
         assert normwise(s, ref) <= F16_NORMWISE, normwise(s, ref)
 
 
+@pytest.mark.parametrize("variant", [
+    dict(mlp="geglu", ffn_dim=768, embed_scale=16.0, attn_scale=0.125),      # Gemma-style
+    dict(mlp="swiglu", ffn_dim=704, attn_scale=0.125),                       # Mistral-style
+    dict(mlp="gelu", ffn_dim=512, attn_scale=0.125),                         # plain, other F
+])
+@pytest.mark.parametrize("dims", ["c1", "odd"])
+@pytest.mark.parametrize("precision", ["f32", "f16"])
+def test_architecture_variants_vs_oracle(variant, dims, precision):
+    """SURVEY §8 f4 (outside reference parity): gated GeGLU / SwiGLU MLPs of
+    width F, Gemma's embedding scale and a softmax scale, against the oracle's
+    restatement of the same architecture, on the tensor-core kernels (c1) and
+    the CUDA-core kernels (odd widths)."""
+    import oracle
+    if dims == "c1":
+        geo = dict(layers=2, model_dim=256, heads=4, kv_heads=2, head_dim=64)
+        D, Q = 128, 48
+    else:
+        geo = dict(layers=2, model_dim=96, heads=3, kv_heads=1, head_dim=32)
+        D, Q = 70, 20
+        variant = dict(variant, ffn_dim=320)
+    cfg = ModelConfig(vocab_size=32768, **geo, **variant)
+    lay = LayoutConfig(document_len=D, query_len=Q)
+    rng = np.random.default_rng(11)
+    docs = rng.integers(1, cfg.vocab_size, (4, D))
+    docs[1, D - 9:] = 0
+    qs = rng.integers(1, cfg.vocab_size, (4, Q))
+    qs[2, Q - 4:] = 0
+    model = krr.RerankModel.build(cfg, lay, precision=precision)
+    kvs = krr.doc_prefill_batch(model, docs, [f"v{i}" for i in range(4)])
+    res, _ = krr.score_batch(model, [("q", k.chunk_id, k, q) for k, q in zip(kvs, qs)], "reuse")
+    s = np.array([r.score for r in res])
+    full, _ = krr.score_batch(model, [("q", f"f{i}", docs[i], qs[i]) for i in range(4)], "full")
+    assert np.array_equal(s, np.array([r.score for r in full]))     # reuse == full, bit-exact
+    ow = oracle.init_weights(oracle.OracleConfig(vocab_size=cfg.vocab_size, document_len=D,
+                                                 query_len=Q, **geo, **variant))
+    if precision == "f16":
+        ow = oracle.round_weights(ow)
+    ref = np.array([oracle.score_full(ow, docs[i], qs[i]) for i in range(4)])
+    if precision == "f32":
+        assert rel_err(s, ref) <= F32_TOL, rel_err(s, ref)
+    else:
+        assert normwise(s, ref) <= F16_NORMWISE, normwise(s, ref)
+
+
 def test_concurrent_score_batch_threads(c1_golden, model_f16):
     """score_batch from several threads at once (the reference's rerank
     workers) gives the same scores as one call."""

@@ -57,6 +57,25 @@ def test_entry_to_f16_pool(g):
     assert np.array_equal(k, want)
 
 
+def test_f16_entries_through_device_store(g, model16):
+    """Scheme code 1 (F16): put lands the exact f16 values in an f16 pool page,
+    get with export_scheme=F16 returns the same bytes (the page itself), and
+    an F32 export of that page decodes to the same values."""
+    cid, k, v, vl = codec.decode_arrays(g["entry_f32"].tobytes())
+    data = codec.encode_arrays(cid, np.array(k), np.array(v), vl, codec.QuantScheme.F16)
+    pool = krr.KVPool(C1[0], 128, 2, "f16")
+    dev = store.DevicePagedKVStore(pool, export_scheme=codec.QuantScheme.F16)
+    dev.put(cid, data)
+    slot = int(pool.lookup([cid])[0])
+    kk, vv = pool.read_host_kv(slot)
+    assert np.array_equal(kk, np.asarray(k).astype(np.float16).astype(np.float32))
+    assert np.array_equal(vv, np.asarray(v).astype(np.float16).astype(np.float32))
+    assert dev.get(cid) == data
+    f32 = codec.encode_pool_page(cid, pool, slot, codec.QuantScheme.F32)
+    _, k3, v3, vl3 = codec.decode_arrays(f32)
+    assert vl3 == vl and np.array_equal(k3, kk) and np.array_equal(v3, vv)
+
+
 def test_device_store_scores_like_reference_entry(g, model32):
     """An F32 entry written by the reference, put into a device shard, scores
     like the oracle on the same KV (f32 debug build, 1e-4 gate)."""

@@ -142,3 +142,28 @@ def test_wide_shapes_vs_reference(golden_dir, name):
     w = oracle.init_weights(cfg, lazy_embedding=True)
     s = [oracle.score_full(w, g["doc_tokens"][i], g["query_tokens"][i]) for i in (0, 1)]
     assert rel_err(s, g["scores"][:2]) <= 1e-4
+
+
+@pytest.mark.parametrize("variant", [dict(mlp="geglu", ffn_dim=96, embed_scale=8.0, attn_scale=0.25),
+                                     dict(mlp="swiglu", ffn_dim=160, attn_scale=0.25)])
+def test_variant_oracle_is_self_consistent(variant):
+    """Architecture variants (outside the reference): defaults
+    reproduce the reference model exactly, a gated MLP is act(x Wg) * (x Wu),
+    the w_gate stream has its own name, and KV reuse == full recompute."""
+    geo = dict(layers=2, model_dim=64, heads=4, kv_heads=2, head_dim=16, vocab_size=4096,
+               document_len=24, query_len=8)
+    base = oracle.init_weights(oracle.OracleConfig(**geo))
+    w = oracle.init_weights(oracle.OracleConfig(**geo, **variant))
+    F = variant["ffn_dim"]
+    assert w.w_up[0].shape == (64, F) and w.w_gate[0].shape == (64, F)
+    assert np.array_equal(w.wqkv[1], base.wqkv[1])            # attention weights unchanged
+    assert not np.array_equal(w.w_gate[0][:, :8], w.w_up[0][:, :8])
+    x = np.random.default_rng(0).standard_normal((3, 64)).astype(np.float32)
+    g, u = x @ w.w_gate[0], x @ w.w_up[0]
+    act = oracle.kvrerank_np._gelu(g) if variant["mlp"] == "geglu" else g / (1 + np.exp(-g))
+    assert np.allclose(oracle.kvrerank_np._mlp(w, 0, x), (act * u) @ w.w_down[0], rtol=1e-6)
+    rng = np.random.default_rng(1)
+    doc, q = rng.integers(1, 4096, 24), rng.integers(1, 4096, 8)
+    k, v, vl = oracle.doc_prefill(w, doc)
+    assert oracle.score_reuse(w, k, v, vl, q) == pytest.approx(oracle.score_full(w, doc, q),
+                                                              rel=1e-5, abs=1e-6)

@@ -46,6 +46,27 @@ def test_f32_decode_is_zero_copy_view(g):
     assert not k.flags.writeable and k.base is not None
 
 
+def test_f16_scheme_roundtrip(g):
+    """Scheme code 1 (this build's F16 extension): payload = the f16-rounded
+    tensors, no scales; decode gives them back exactly as f32."""
+    cid, k, v, vl = codec.decode_arrays(g["entry_f32"].tobytes())
+    data = codec.encode_arrays(cid, np.array(k), np.array(v), vl, S.F16)
+    L, KVH, D, HD = k.shape
+    assert len(data) == codec.HEADER.size + len(cid) + codec.payload_nbytes(L, KVH, D, HD, S.F16)
+    assert data[6] == 1
+    cid2, k2, v2, vl2 = codec.decode_arrays(data)
+    assert (cid2, vl2) == (cid, vl)
+    assert np.array_equal(k2, np.asarray(k).astype(np.float16).astype(np.float32))
+    assert np.array_equal(v2, np.asarray(v).astype(np.float16).astype(np.float32))
+    # f16-exact inputs survive unchanged; out-of-range values are refused
+    assert codec.encode_arrays(cid, k2, v2, vl, S.F16) == data
+    big = np.array(k); big[0, 0, 0, 0] = 1e6
+    with pytest.raises(CodecError):
+        codec.encode_arrays(cid, big, np.array(v), vl, S.F16)
+    with pytest.raises(CodecError):
+        codec.quantize_tensor(np.zeros((1, 2, 2), np.float32), S.F16)
+
+
 @pytest.mark.parametrize("name", ["int8", "int4"])
 def test_quantize_edge_cases_vs_reference(g, name):
     q, sc = codec.quantize_tensor(g["edge_tensor"], codec.QuantScheme.from_name(name))
@@ -66,6 +87,7 @@ def test_quant_error_bound(scheme):
 def test_payload_sizes():
     # SURVEY §4 closed forms (default config L=4, KVH=2, D=256, HD=16)
     assert codec.payload_nbytes(4, 2, 256, 16, S.F32) == 262144
+    assert codec.payload_nbytes(4, 2, 256, 16, S.F16) == 131072
     assert codec.payload_nbytes(4, 2, 256, 16, S.INT8_PER_CHANNEL) == 65536
     assert codec.payload_nbytes(4, 2, 256, 16, S.INT4_PER_CHANNEL) == 32768
     assert codec.payload_nbytes(1, 1, 3, 1, S.INT4_PER_CHANNEL) == 4   # odd count pads
@@ -81,8 +103,11 @@ def test_format_errors(g):
     bad = bytearray(data); bad[4] = 9
     with pytest.raises(FormatError):
         codec.decode_arrays(bytes(bad))
-    bad = bytearray(data); bad[6] = 1          # scheme code 1 is unused in the reference
+    bad = bytearray(data); bad[6] = 7          # no such scheme code
     with pytest.raises(FormatError):
+        codec.decode_arrays(bytes(bad))
+    bad = bytearray(data); bad[6] = 1          # F16 header over an INT8-sized body
+    with pytest.raises(CodecError):
         codec.decode_arrays(bytes(bad))
     with pytest.raises(CodecError):
         codec.decode_arrays(bytes(data[:-1]))
@@ -95,7 +120,8 @@ def test_format_errors(g):
 
 def test_scheme_names():
     assert S.from_name("kv8") is S.INT8_PER_CHANNEL and S.from_name(" INT4 ") is S.INT4_PER_CHANNEL
-    assert [s.short_name for s in S] == ["f32", "int8", "int4"]
+    assert [s.short_name for s in S] == ["f32", "f16", "int8", "int4"]
+    assert S.from_name("half") is S.F16 and not S.F16.quantised and S.INT4_PER_CHANNEL.quantised
 
 
 # ------------------------------------------------------------------ store

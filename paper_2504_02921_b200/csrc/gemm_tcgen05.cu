@@ -570,11 +570,17 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
     const char* e = getenv("KRR_GEMM_NARROW");
     narrow = e ? atoi(e) : 1;
   }
+  static int force_bn = -1;                 // KRR_GEMM_BN=256|128|64: experiments only
+  if (force_bn < 0) {
+    const char* e = getenv("KRR_GEMM_BN");
+    force_bn = e && (atoi(e) == 64 || atoi(e) == 128 || atoi(e) == 256) ? atoi(e) : 0;
+  }
   int bn = BN;
   if (narrow && (mode == 1 || mode == 4)) {
     const int64_t num_m = (M + 127) / 128;
     while (bn > 64 && num_m * ((N + bn - 1) / bn) < device_sm_count()) bn /= 2;
   }
+  if (force_bn && (mode == 1 || mode == 4)) bn = force_bn;
   CUtensorMap ma, mb, mo;
   int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;

@@ -66,6 +66,8 @@ for quant in (None, "int8", "int4"):
                 issue(gi + 2)
         t1 = ev(); t1.record()
         torch.cuda.synchronize()
+        print(f"  rep{rep}: step {t0.elapsed_time(t1):.1f} ms; score per group " +
+              " ".join(f"{m[3].elapsed_time(m[4]):.1f}" for m in marks), flush=True)
     tot = t0.elapsed_time(t1)
     torch.cuda.synchronize()
     t2 = time.perf_counter()

@@ -18,7 +18,7 @@ echo "ncu attn rc=$?"
 timeout -s KILL 1500 python bench.py --config c4 --steps 3 --warmup 2 --latency-reps 5 --no-cpu-baseline > gpurun_out/${TAG}_c4.json 2> gpurun_out/${TAG}_c4.err
 echo "c4 rc=$?"; python scripts/show.py gpurun_out/${TAG}_c4.json; tail -2 gpurun_out/${TAG}_c4.err
 for qz in "" int8 int4; do
-  timeout -s KILL 900 python bench.py --config c5 --steps 3 --warmup 1 --query-lens 16,48,256 --no-cpu-baseline ${qz:+--host-quant $qz} > gpurun_out/${TAG}_c5_${qz:-f16}.json 2> gpurun_out/${TAG}_c5_${qz:-f16}.err
+  timeout -s KILL 900 python bench.py --config c5 --steps 3 --warmup 2 --query-lens 16,48,256 --no-cpu-baseline ${qz:+--host-quant $qz} > gpurun_out/${TAG}_c5_${qz:-f16}.json 2> gpurun_out/${TAG}_c5_${qz:-f16}.err
   echo "c5 ${qz:-f16} rc=$?"
 done
 timeout -s KILL 900 python bench.py --config c2 --steps 20 --warmup 3 --latency-reps 15 > gpurun_out/${TAG}_c2.json 2> gpurun_out/${TAG}_c2.err

@@ -136,7 +136,8 @@ def cpu_pairs_per_s(preset, D, Q, budget_s=12.0, max_pairs=8):
     ocfg = oracle.OracleConfig(layers=cfg.layers, model_dim=cfg.model_dim, heads=cfg.heads,
                                kv_heads=cfg.kv_heads, head_dim=cfg.head_dim,
                                vocab_size=cfg.vocab_size, max_position=cfg.max_position,
-                               document_len=D, query_len=Q)
+                               document_len=D, query_len=Q, mlp=cfg.mlp, ffn_dim=cfg.ffn_dim,
+                               embed_scale=cfg.embed_scale, attn_scale=cfg.attn_scale)
     rng = np.random.default_rng(3)
     per_layer = cfg.model_dim >= 1024
     if per_layer:

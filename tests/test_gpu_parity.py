@@ -313,3 +313,25 @@ def test_concurrent_score_batch_threads(c1_golden, model_f16):
         t.join()
     for g in got:
         assert [r.score for r in g] == [r.score for r in want]
+
+
+def test_entry_point_errors(c1_golden, model_f16):
+    """The public entry points raise the reference's error classes
+    (reranker.py:146-151, 154-179, 241-249, 265-290)."""
+    from paper_2504_02921_b200.errors import ConfigError, DegenerateInputError, ShapeError
+    docs, q = c1_golden["doc_tokens"][:1], c1_golden["query_tokens"]
+    kv = krr.doc_prefill_batch(model_f16, docs, ["e0"])[0]
+    with pytest.raises(ShapeError):
+        krr.score_reuse(model_f16, kv, q[:-1])
+    with pytest.raises(DegenerateInputError):
+        krr.score_reuse(model_f16, kv, np.zeros_like(q))
+    with pytest.raises(ConfigError):
+        krr.score_reuse(model_f16, kv, q, path="fused")
+    with pytest.raises(ShapeError):
+        krr.score_full(model_f16, docs[0][:-1], q)
+    with pytest.raises(DegenerateInputError):
+        krr.score_full(model_f16, np.zeros_like(docs[0]), q)
+    with pytest.raises(ConfigError):
+        krr.score_batch(model_f16, [("q", "e0", kv, q)], mode="bogus")
+    with pytest.raises(ShapeError):
+        krr.score_batch(model_f16, [("q", "e0", docs[0], q)], mode="reuse")

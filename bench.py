@@ -568,7 +568,7 @@ def main():
     ap.add_argument("--full-pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--query-lens", default="", help="C5 sweep, e.g. 16,32,48,64,128,256")
-    ap.add_argument("--staging-slots", type=int, default=32,
+    ap.add_argument("--staging-slots", type=int, default=16,
                     help="C5: HBM staging slots (two halves, double-buffered)")
     ap.add_argument("--host-quant", default="", choices=["", "int8", "int4"],
                     help="C5: keep host-tier pages HRKV-quantised (2x/4x fewer PCIe bytes)")

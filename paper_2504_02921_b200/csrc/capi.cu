@@ -417,10 +417,11 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
     static int which = -1;
     if (which < 0) {
       const char* e = getenv("KRR_ATTN_TC_KERNEL");
-      which = !e ? 0 : (!strcmp(e, "pp") ? 1 : !strcmp(e, "v1") ? 2 : 0);
+      which = !e ? 0 : (!strcmp(e, "pp") ? 1 : !strcmp(e, "v1") ? 2 : !strcmp(e, "fa2") ? 3 : 0);
     }
     if (which == 2 || p.head_dim == 256) return launch_attention_tcgen05(act, p, s);
     if (which == 1) return launch_attention_pingpong(act, p, s);
+    if (which == 3) return launch_attention_fa2(act, p, s);
     return launch_attention_fa(act, p, s);
   }
   if (backend == KRR_ATTN_MMA) return launch_attention_mma(act, p, s);

@@ -202,12 +202,16 @@ def run_reference(args, rank, world):
 
 
 def workload_config(args, cfg, lay, corpus, nq, nc, keep):
-    return {"workload": f"{CONFIGS[args.config][0]}: {nq} queries x {nc * args.gpus} docs x "
-                        f"{lay.document_len} tok, query suffix {lay.query_len}, "
-                        f"corpus {corpus} docs/GPU HBM-resident",
+    strong = getattr(args, "scaling", "weak") == "strong"
+    n_cand = nc if strong else nc * args.gpus
+    where = (f"one {corpus}-doc corpus sharded by doc id over {args.gpus} GPU(s)" if strong
+             else f"corpus {corpus} docs/GPU HBM-resident")
+    return {"workload": f"{CONFIGS[args.config][0]}: {nq} queries x {n_cand} docs x "
+                        f"{lay.document_len} tok, query suffix {lay.query_len}, {where}",
+            "scaling_mode": "strong" if strong else "weak",
             "layers": cfg.layers, "model_dim": cfg.model_dim, "heads": cfg.heads,
             "kv_heads": cfg.kv_heads, "head_dim": cfg.head_dim, "mlp": "gelu_tanh 4d",
-            "queries": nq, "candidates_per_query": nc * args.gpus, "doc_len": lay.document_len,
+            "queries": nq, "candidates_per_query": n_cand, "doc_len": lay.document_len,
             "query_len": lay.query_len, "corpus_docs_per_gpu": corpus, "keep": keep,
             "parallelism": f"doc-shard x{args.gpus} + NCCL all-gather top-k"
             if args.gpus > 1 else "1 GPU",
@@ -355,32 +359,60 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
 
-    # ---- corpus shard: docs with global id rank*corpus + i, prefilled into the HBM pool
-    pool = krr.KVPool(cfg, D, corpus, w.dtype, dev)
-    rng = np.random.default_rng(1000 + rank)
-    docs = rng.integers(1, cfg.vocab_size, (corpus, D), dtype=np.int64)
-    ids = [f"doc-{rank * corpus + i:06d}" for i in range(corpus)]
+    strong = args.scaling == "strong"
+    if strong:
+        # strong scaling: ONE corpus of `corpus` docs, rank r holds
+        # the docs with index % world == r; the same queries and candidate lists
+        # on every rank, each rank scores the pairs whose document it owns
+        all_docs = np.random.default_rng(1000).integers(1, cfg.vocab_size, (corpus, D),
+                                                        dtype=np.int64)
+        owned = np.nonzero(shard.owner_of(np.arange(corpus), world) == rank)[0]
+        docs = all_docs[owned]
+        ids = [f"doc-{i:06d}" for i in owned]
+        del all_docs
+    else:
+        # weak scaling: each rank its own corpus shard, global ids rank*corpus + i
+        rng = np.random.default_rng(1000 + rank)
+        docs = rng.integers(1, cfg.vocab_size, (corpus, D), dtype=np.int64)
+        ids = [f"doc-{rank * corpus + i:06d}" for i in range(corpus)]
+    n_docs = len(ids)
+    pool = krr.KVPool(cfg, D, n_docs, w.dtype, dev)
     slots = pool.allocate(ids)
-    engine.prefill_slots(w, pool, slots, docs, np.full(corpus, D))  # warm-up / compile
+    engine.prefill_slots(w, pool, slots, docs, np.full(n_docs, D))  # warm-up / compile
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    engine.prefill_slots(w, pool, slots, docs, np.full(corpus, D))
+    engine.prefill_slots(w, pool, slots, docs, np.full(n_docs, D))
     torch.cuda.synchronize()
     prefill_s = time.perf_counter() - t0
 
     # ---- queries (broadcast: same on every rank) and per-rank candidates
     qrng = np.random.default_rng(7)
     q_host = qrng.integers(1, cfg.vocab_size, (nq, Q), dtype=np.int64)
-    crng = np.random.default_rng(100 + rank)
-    cand_local = np.stack([crng.choice(corpus, nc, replace=False) for _ in range(nq)])
-    cand_ids = [[ids[j] for j in row] for row in cand_local]
     q_dev = torch.as_tensor(q_host.astype(np.int32), device=dev)
-    slots_dev = torch.as_tensor(slots[cand_local.reshape(-1)], device=dev)
-    qidx = torch.arange(nq, device=dev).repeat_interleave(nc)
-    gid_dev = torch.as_tensor((rank * corpus + cand_local).reshape(-1).astype(np.int32),
-                              device=dev)
     k = min(keep, nc)
-    scores = torch.empty(nq * nc, dtype=torch.float32, device=dev)
+    if strong:
+        crng = np.random.default_rng(100)
+        cand_g = np.stack([crng.choice(corpus, nc, replace=False) for _ in range(nq)])
+        work = shard.local_work(cand_g, rank, world)
+        slot_of = np.full(corpus, -1, dtype=np.int64)
+        slot_of[owned] = slots
+        pair_doc = cand_g[work.pair_query, work.pair_cand]
+        n_local = int(pair_doc.size)
+        slots_dev = torch.as_tensor(slot_of[pair_doc], device=dev)
+        qidx = torch.as_tensor(work.pair_query, device=dev)
+        gid_dev = torch.as_tensor(pair_doc.astype(np.int32), device=dev)
+        mine = shard.owner_of(cand_g, world) == rank
+        cand_ids = [[f"doc-{d:06d}" for d in cand_g[q][mine[q]]] for q in range(nq)]
+    else:
+        crng = np.random.default_rng(100 + rank)
+        cand_local = np.stack([crng.choice(corpus, nc, replace=False) for _ in range(nq)])
+        cand_ids = [[ids[j] for j in row] for row in cand_local]
+        n_local = nq * nc
+        slots_dev = torch.as_tensor(slots[cand_local.reshape(-1)], device=dev)
+        qidx = torch.arange(nq, device=dev).repeat_interleave(nc)
+        gid_dev = torch.as_tensor((rank * corpus + cand_local).reshape(-1).astype(np.int32),
+                                  device=dev)
+    scores = torch.empty(n_local, dtype=torch.float32, device=dev)
 
     def merge(idx, sc):
         """Global top-k: one all-gather of per-rank (score, doc id), merged on
@@ -390,6 +422,8 @@ def run_ours(args, rank, world, local_rank):
 
     def step():
         engine.score_slots(w, pool, slots_dev, q_dev.index_select(0, qidx), out=scores)
+        if strong:       # ragged local segments: local top-k, then the one all-gather
+            return shard.sharded_select(scores, gid_dev, work, nq, k, engine.segmented_topk)
         idx, sc = engine.segmented_topk(scores, gid_dev, nq, nc, k)
         return merge(idx, sc)
 
@@ -421,16 +455,17 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    pairs_step = nq * nc * world
+    pairs_step = nq * nc * (1 if strong else world)
     value = pairs_step * args.steps / (ms / 1e3)
 
     # ---- e2e through the public API (host inputs -> host top-k), max over ranks
     def e2e_step():
         res = pipeline.rerank(model, pool, [f"q{i}" for i in range(nq)], q_host, cand_ids, k)
-        if world > 1:
-            sc = torch.tensor([[p.score for p in r] for r in res.selected], device=dev)
-            gi = torch.tensor([[int(p.chunk_id[4:]) for p in r] for r in res.selected],
-                              dtype=torch.int32, device=dev)
+        if world > 1:       # pad ragged local top-k lists to k before the merge
+            sc = torch.tensor([[p.score for p in r] + [float("-inf")] * (k - len(r))
+                               for r in res.selected], device=dev)
+            gi = torch.tensor([[int(p.chunk_id[4:]) for p in r] + [shard.PAD_ID] * (k - len(r))
+                               for r in res.selected], dtype=torch.int32, device=dev)
             mi, _ = shard.merge_topk(sc, gi, k, engine.segmented_topk)
             mi.cpu()
         return res
@@ -464,9 +499,10 @@ def run_ours(args, rank, world, local_rank):
         lat_g = []
         if args.latency_reps:
             try:
-                gs = engine.GraphedScorer(w, pool, 1, nc, Q, k)
+                n1 = len(cand_ids[0])
+                gs = engine.GraphedScorer(w, pool, 1, n1, Q, min(k, n1))
                 sl1 = pool.lookup(cand_ids[0])
-                ranks = np.arange(nc, dtype=np.int32)
+                ranks = np.arange(n1, dtype=np.int32)
                 for i in range(args.latency_reps + 2):
                     torch.cuda.synchronize()
                     t0 = time.perf_counter()
@@ -504,7 +540,7 @@ def run_ours(args, rank, world, local_rank):
                 tj = json.load(f)
             traffic, traffic_alg = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
         # attention kernel: cached-KV bytes it must read per step at HBM bandwidth
-        attn_bytes = nq * nc * kv_bytes_per_pair(cfg, D)
+        attn_bytes = n_local * kv_bytes_per_pair(cfg, D)
         attn_gbs = attn_bytes / (prof["attn_ms"] / args.steps / 1e3) / 1e9 if prof["attn_ms"] else 0
         cpu = None
         if not args.no_cpu_baseline:
@@ -514,7 +550,7 @@ def run_ours(args, rank, world, local_rank):
         out = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic (reference random-init weights, seed 0; "
                                               "uniform token ids)",
             "config": workload_config(args, cfg, lay, corpus, nq, nc, keep),
@@ -538,11 +574,11 @@ def run_ours(args, rank, world, local_rank):
                                        "bytes_per_step": attn_bytes}},
             "cpu_baseline": cpu,
             "p50_query_latency_ms": float(np.median(lat)) if lat else None,
-            "p50_query_latency_candidates": nc,
+            "p50_query_latency_candidates": len(cand_ids[0]),
             "p50_query_latency_graph_ms": float(np.median(lat_g)) if lat_g else None,
             "full_recompute_pairs_per_s": full_pps,
             "reuse_over_full": value / world / full_pps,
-            "prefill_docs_per_s": corpus / prefill_s,
+            "prefill_docs_per_s": n_docs / prefill_s,
             "hbm": {"kv_pool_gb": pool.slab.numel() * pool.slab.element_size() / 1e9,
                     "weights_gb": w.nbytes() / 1e9,
                     "max_allocated_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
@@ -556,6 +592,10 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU its own corpus shard and candidate lists (default); "
+                         "strong: one corpus sharded by doc id, the same candidates split "
+                         "across GPUs (SURVEY §8(d) protocol)")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

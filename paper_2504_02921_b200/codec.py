@@ -308,7 +308,7 @@ def decode_entry_to_pool(data, pool, slot: int | None = None, stream=None):
             page.copy_(src.to(dev, non_blocking=False).view(page.shape))
         else:
             codes = torch.frombuffer(bytearray(v.payload()), dtype=torch.uint8).to(dev)
-            scales = torch.from_numpy(np.ascontiguousarray(v.scales())).to(dev)
+            scales = torch.from_numpy(np.array(v.scales(), dtype=np.float32)).to(dev)
             L_ = _lib.lib()
             for li in range(L):
                 for j in range(2):

@@ -121,3 +121,22 @@ def test_id_ranks_follow_chunk_id_order():
     s = [krr.ScoredPair("b", "q", 1.0), krr.ScoredPair("a", "q", 1.0),
          krr.ScoredPair("c", "q", 2.0)]
     assert [p.chunk_id for p in select(s, 2)] == ["c", "a"]
+
+
+def test_header_enums_match_host_constants():
+    """The C-ABI enum values (include/kvrerank_b200.h) and the ctypes host layer
+    agree: dtypes, epilogues, MLP kinds, backends."""
+    import re
+    src = open(os.path.join(ROOT, "include", "kvrerank_b200.h")).read()
+    vals = {m.group(1): int(m.group(2)) for m in re.finditer(r"\b(KRR_[A-Z0-9_]+)\s*=\s*(\d+)", src)}
+    want = {"KRR_F32": _lib.F32, "KRR_F16": _lib.F16, "KRR_BF16": _lib.BF16,
+            "KRR_EPI_STORE": _lib.EPI_STORE, "KRR_EPI_GELU": _lib.EPI_GELU,
+            "KRR_EPI_RESIDUAL": _lib.EPI_RESIDUAL, "KRR_EPI_QKV_ROPE": _lib.EPI_QKV_ROPE,
+            "KRR_EPI_GLU_GELU": _lib.EPI_GLU_GELU, "KRR_EPI_GLU_SILU": _lib.EPI_GLU_SILU,
+            "KRR_MLP_GELU": _lib.MLP_GELU, "KRR_MLP_GEGLU": _lib.MLP_GEGLU,
+            "KRR_MLP_SWIGLU": _lib.MLP_SWIGLU, "KRR_GEMM_AUTO": _lib.GEMM_AUTO,
+            "KRR_GEMM_TCGEN05": _lib.GEMM_TCGEN05, "KRR_GEMM_SIMT": _lib.GEMM_SIMT,
+            "KRR_ATTN_AUTO": _lib.ATTN_AUTO, "KRR_ATTN_MMA": _lib.ATTN_MMA,
+            "KRR_ATTN_SIMT": _lib.ATTN_SIMT, "KRR_ATTN_TCGEN05": _lib.ATTN_TCGEN05}
+    for name, v in want.items():
+        assert vals.get(name) == v, (name, vals.get(name), v)

@@ -46,6 +46,10 @@ namespace tc {
 
 constexpr int BN = 256, BK = 64;
 constexpr int THREADS = 192;
+// CG=5 drains a single-buffered 256x256 accumulator: 8 epilogue warps (two per
+// TMEM lane quadrant, one per 128-row half) halve the exposed epilogue
+template <int CG> constexpr int threads() { return CG == 5 ? 320 : THREADS; }
+template <int CG> constexpr int epi_warps() { return CG == 5 ? 8 : 4; }
 constexpr int STG_BUF = 4096;                 // one 32x32 chunk (f32) per buffer
 constexpr int STG_WARP_BYTES = 2 * STG_BUF;   // double buffered per epilogue warp
 
@@ -76,8 +80,20 @@ template <> struct Cfg<4> {
   static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 256 * BK * 2;
   static constexpr int B_ROWS = 64;
 };
+// CG=5: as CG=3 but each CTA owns 256 rows (two M=128 MMAs per k-step share
+// one B stage, into TMEM columns 0-255 and 256-511): per CTA and k-block
+// 32 KB of A + 32 KB of B for 8.4 MFLOP instead of 48 KB per 4.2 MFLOP, at the
+// price of a single-buffered accumulator (the epilogue of a tile is not
+// overlapped with the next tile's main loop).
+template <> struct Cfg<5> {
+  static constexpr int TILE_M = 512, STAGES = 3, GROUP_M = 4;
+  static constexpr int A_BYTES = 256 * BK * 2, B_BYTES = 256 * BK * 2;
+  static constexpr int B_ROWS = 128;
+};
 // CTAs per cluster: 1 (CG=1), 2 (cta_group::2 pair, or B multicast), 4 (B multicast)
 template <int CG> constexpr int cluster_size() { return CG == 1 ? 1 : CG == 4 ? 4 : 2; }
+// rows of A per CTA (two M=128 MMAs per k-step for CG=5)
+template <int CG> constexpr int cta_rows() { return CG == 5 ? 256 : 128; }
 template <int CG> constexpr bool multicast_b() { return CG >= 3; }
 template <int CG>
 constexpr int smem_bytes() {
@@ -230,9 +246,45 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap
   __syncwarp();
 }
 
+// Direct epilogue (CG=5): no shared-memory staging and no TMA store, so a
+// single-buffered accumulator drains without waiting on bulk-store completion.
+// Thread `lane` owns row row0+lane, columns col0..col0+31 (64 B of 16-bit
+// output or 128 B of f32 residual, contiguous per thread).
+template <typename T>
+__device__ __forceinline__ void epi_direct(const EpiParams& ep, const uint32_t (&r)[32],
+                                           int64_t row0, int lane, int col0) {
+  const int64_t row = row0 + lane;
+  if (row >= ep.M) return;
+  if (ep.kind == KRR_EPI_RESIDUAL) {
+    float4* x = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + row * ep.N + col0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 o = x[j];
+      o.x += __uint_as_float(r[4 * j]);
+      o.y += __uint_as_float(r[4 * j + 1]);
+      o.z += __uint_as_float(r[4 * j + 2]);
+      o.w += __uint_as_float(r[4 * j + 3]);
+      x[j] = o;
+    }
+    return;
+  }
+  uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<T*>(ep.out) + row * ep.N + col0);
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (ep.kind == KRR_EPI_GELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    o[j] = make_uint4(pack16<T>(v[8 * j], v[8 * j + 1]), pack16<T>(v[8 * j + 2], v[8 * j + 3]),
+                      pack16<T>(v[8 * j + 4], v[8 * j + 5]), pack16<T>(v[8 * j + 6], v[8 * j + 7]));
+}
+
 // ------------------------------------------------------------ kernel
 template <typename T, int CG>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(threads<CG>(), 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmOut, int64_t M, int N, int K,
@@ -264,7 +316,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], multicast_b<CG>() ? cluster_size<CG>() : 1);
     }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4 * MMA_CG); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], epi_warps<CG>() * MMA_CG);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -310,7 +365,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_expect_tx(&full[stage], C::A_BYTES + bn * BK * 2);
             const uint32_t bar = smem_u32(&full[stage]);
             tma_load<1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
-                        mb * C::TILE_M + (int)rank * 128);
+                        mb * C::TILE_M + (int)rank * cta_rows<CG>());
             tma_load_mc(sB + stage * C::B_BYTES + rank * (b_rows * BK * 2), &tmB, bar,
                         kb * BK, nb * bn + (int)rank * b_rows, MC_MASK);
           } else {
@@ -339,8 +394,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t dA = sw128_desc(smem_u32(sA));
       const uint64_t dB = sw128_desc(smem_u32(sB));
       for (int tile = cid; tile < tiles; tile += ncl, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        // CG=5 uses both 256-column halves for one tile (rows 0-127 / 128-255)
+        const int acc = CG == 5 ? 0 : (it & 1);
+        const uint32_t acc_phase = CG == 5 ? (it & 1) : ((it >> 1) & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;   // accumulators 256 columns apart
@@ -349,9 +405,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_fence_after();
           if (elect_one_sync()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
+            for (int k = 0; k < BK / 16; ++k) {
               mma_f16<MMA_CG>(d_tmem, dA + ((stage * C::A_BYTES + k * 32) >> 4),
                               dB + ((stage * C::B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+              if constexpr (CG == 5)   // rows 128-255: A + 128 rows x 128 B, TMEM + 256 columns
+                mma_f16<MMA_CG>(d_tmem + BN, dA + ((stage * C::A_BYTES + 128 * 128 + k * 32) >> 4),
+                                dB + ((stage * C::B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+            }
             if constexpr (multicast_b<CG>()) mma_commit_mc1(&empty[stage], MC_MASK);
             else mma_commit<MMA_CG>(&empty[stage]);
           }
@@ -364,7 +424,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    uint8_t* stg = stage_base + (warp - 2) * STG_WARP_BYTES;
+    // CG=5: 8 warps share the 4-warp staging area (one 4 KB buffer each; only
+    // the QKV scatter uses it there)
+    uint8_t* stg = stage_base + (warp - 2) * (CG == 5 ? STG_BUF : STG_WARP_BYTES);
+    const int epi_half = CG == 5 ? (warp - 2) >> 2 : 0;   // CG=5: 128-row half this warp drains
     const uint32_t tempty0 =
         CG == 2 ? mapa_rank(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     int it = 0, nchunk = 0;
@@ -373,19 +436,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       int mb, nb;
       tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = CG == 5 ? 0 : (it & 1);
+      const uint32_t acc_phase = CG == 5 ? (it & 1) : ((it >> 1) & 1);
       // one epilogue warp polls the accumulator barrier; the other three are
       // parked on a named barrier (the poll loop of four warps was ~1/4 of all
       // issued instructions and power)
       if (warp == 2) mbar_wait(&tfull[acc], acc_phase);
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 32 * epi_warps<CG>());
       tc_fence_after();
-      const int64_t row0 = (int64_t)mb * C::TILE_M + rank * 128 + quad * 32;
+      // CG=5: the tile's second 128 rows live in TMEM columns 256-511
 #pragma unroll 1
-      for (int c = 0; c < bn / 32; ++c) {
+      for (int cc = 0; cc < bn / 32; ++cc) {
+        const int h = epi_half, c = cc;
+        const int64_t row0 = (int64_t)mb * C::TILE_M + rank * cta_rows<CG>() + h * 128 + quad * 32;
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (acc + h) * BN + c * 32, r);
         int col0 = nb * bn + c * 32;
         if (col0 >= N) continue;
         if (glu) {
@@ -402,7 +467,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(gate[j] * __uint_as_float(r[j]));
           col0 = (col0 - 32) / 2;
         }
-        uint8_t* buf = stg + (nchunk & 1) * STG_BUF;
+        if constexpr (CG == 5) {
+          if (ep.kind != KRR_EPI_QKV_ROPE) {
+            epi_direct<T>(ep, r, row0, lane, col0);
+            continue;
+          }
+        }
+        uint8_t* buf = stg + (CG == 5 ? 0 : (nchunk & 1) * STG_BUF);
         ++nchunk;
         // the bulk op that last read this buffer (two chunks ago) must be done
         if (lane == 0) bulk_wait_read<1>();
@@ -496,7 +567,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + bn - 1) / bn);
   constexpr int CS = cluster_size<CG>();
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(threads<CG>());
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];
@@ -548,13 +619,16 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   //      by TMA multicast (DEFAULT: 2/3 of the L2->SM traffic of mode 1; under
   //      the power cap this buys ~6% higher clocks, +6% pairs/s on C3)
   //   5  as 4 with clusters of 4 (measured much slower)
+  //   6  as 4 with 256 rows per CTA (Cfg<5>: two MMAs per k-step share one B
+  //      stage); launches with M < 8192 use mode 4
   static int env_mode = -1;
   if (env_mode < 0) {
     const char* e = getenv("KRR_GEMM_CTA");
     env_mode = e ? atoi(e) : 4;
-    if (env_mode < 1 || env_mode > 5) env_mode = 4;
+    if (env_mode < 1 || env_mode > 6) env_mode = 4;
   }
   int mode = env_mode == 3 ? (K <= 4096 && M >= 1024 ? 2 : 1) : env_mode;
+  if (mode == 6 && M < 8192) mode = 4;
   if (mode == 4 && M <= 128) mode = 1;   // one 128-row tile: a cluster partner would idle
   const CUtensorMapDataType dt =
       act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -596,10 +670,11 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   }
   if (force_bn && (mode == 1 || mode == 4)) bn = force_bn;
   CUtensorMap ma, mb, mo;
-  int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, mode == 6 ? 256 : 128,
+                    CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK,
-                mode == 5 ? 64 : mode == 2 ? 128 : mode == 4 ? bn / 2 : bn,
+                mode == 5 ? 64 : mode == 2 ? 128 : (mode == 4 || mode == 6) ? bn / 2 : bn,
                 CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   if (ep.kind == KRR_EPI_RESIDUAL) {
@@ -623,10 +698,12 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
                          ((uint32_t)(tile_m >> 4) << 24);
   if (act_dtype == KRR_F16)
     return mode == 2   ? launch<__half, 2>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+           : mode == 6 ? launch<__half, 5>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
            : mode == 4 ? launch<__half, 3>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
            : mode == 5 ? launch<__half, 4>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
                        : launch<__half, 1>(ma, mb, mo, M, N, K, idesc, bn, ep, s);
   return mode == 2   ? launch<__nv_bfloat16, 2>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
+         : mode == 6 ? launch<__nv_bfloat16, 5>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
          : mode == 4 ? launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
          : mode == 5 ? launch<__nv_bfloat16, 4>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
                      : launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, bn, ep, s);

@@ -146,7 +146,11 @@ uint64_t krr_launch_count(void);          /* kernels launched by this library so
 /* Bytes of scratch krr_forward needs for n_seqs*seq_len rows. */
 int krr_workspace_bytes(const krr_model_t* m, int64_t rows, size_t* out_bytes);
 
-/* Full layer stack over a batch (embedding -> L layers -> final norm/score). */
+/* Full layer stack over a batch (embedding -> L layers -> final norm/score).
+ * Replaces kvrerank/model.py:332-403 `forward` as called per pair by
+ * reranker.py:182-201 (`doc_prefill`, prefix_len = 0: K/V written into pool
+ * pages) and :204-212 (`_query_block`, prefix_len = D: suffix scoring), batched
+ * over all pairs in one M dimension. */
 int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace,
                 size_t workspace_bytes, krr_stream_t stream);
 
@@ -156,15 +160,23 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace,
 int krr_profile_enable(int enable);
 int krr_profile_read(double* ms_out3, uint64_t* launches_out3, double* gemm_flops_out);
 
+/* model.py:123-129 `_tensor` / hashing.py:58-80 `uniform_signed`: one named
+ * SplitMix64 stream, written K-major ([out, in]) when transpose != 0. */
 int krr_init_uniform(uint64_t stream_seed, double bound, int64_t rows, int64_t cols,
                      int transpose, int out_dtype, void* out, int64_t out_ld,
                      krr_stream_t stream);
+/* model.py:352 token-embedding gather (f32 residual stream). */
 int krr_embed(const int32_t* tokens, const float* emb, int64_t rows, int32_t d,
               float* x, krr_stream_t stream);
+/* model.py:439-441 `_norm_rows` (x / sqrt(mean x^2 + eps) * gain). */
 int krr_rmsnorm(const float* x, const float* gain, int64_t rows, int32_t d, int out_dtype,
                 void* out, krr_stream_t stream);
+/* model.py:368 (x @ wqkv + RoPE :370-371 + GQA pack :377-378), :397 (attn @ wo
+ * + residual), :399-400 (gelu(xn @ w_up) @ w_down + residual); epilogue per KRR_EPI_*. */
 int krr_gemm(int backend, int act_dtype, const void* A, const void* B, int64_t M, int32_t N,
              int32_t K, int epilogue, void* out, const krr_qkv_t* qkv, krr_stream_t stream);
+/* model.py:373-394 attention over cached prefix K/V + causal suffix, with
+ * `_exp_rows` :406-436 (shared max, masked rows -> 0, no 1/sqrt(HD)). */
 int krr_attention(int backend, int act_dtype, const void* q, int32_t n_seqs, int32_t kv_heads,
                   int32_t group, int32_t head_dim, int32_t seq_len, int32_t prefix_len,
                   int32_t layer, int32_t cur_layer, void* const* prefix_kv,
@@ -172,12 +184,14 @@ int krr_attention(int backend, int act_dtype, const void* q, int32_t n_seqs, int
                   const uint8_t* tok_valid, void* out, const void* prefix_pool,
                   int64_t prefix_pool_bytes, const void* cur_pool, int64_t cur_pool_bytes,
                   krr_stream_t stream);
-/* Co-resident CTAs per SM of the tcgen05 attention kernel (design point: 2). */
+/* Co-resident CTAs per SM of the tcgen05 attention kernel (diagnostic). */
 int krr_attention_occupancy(int act_dtype, int32_t head_dim, int32_t* ctas_per_sm);
+/* model.py:402 final norm + reranker.py:211-212 score of the last valid row
+ * (the reference's d-vector head, or the yes/no lm_head-row difference). */
 int krr_score_head(const float* x, int32_t n_seqs, int32_t seq_len, int32_t d,
                    const int32_t* last_index, const float* final_gain, const float* head,
                    float* scores, krr_stream_t stream);
-/* Top-k per segment by (score desc, doc_id asc).  scores/doc_ids [n_seg*seg_len];
+/* pipeline.py:285-287 `_select`: top-k per segment by (score desc, doc_id asc).  scores/doc_ids [n_seg*seg_len];
  * out_idx [n_seg*k] (index within segment, -1 when k > seg_len). */
 int krr_segmented_topk(const float* scores, const int32_t* doc_ids, int32_t n_seg,
                        int32_t seg_len, int32_t k, int32_t* out_idx, float* out_score,

@@ -444,7 +444,49 @@ __global__ void __launch_bounds__(threads<CG>(), 1)
       if (warp == 2) mbar_wait(&tfull[acc], acc_phase);
       named_bar_sync(1, 32 * epi_warps<CG>());
       tc_fence_after();
-      // CG=5: the tile's second 128 rows live in TMEM columns 256-511
+      if constexpr (CG == 5) {
+        // this warp's 128-row half: TMEM loads software-pipelined one chunk
+        // ahead of the processing (the single-buffered accumulator's drain is
+        // on the critical path)
+        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (acc + epi_half) * BN;
+        const int64_t row0 = (int64_t)mb * C::TILE_M + rank * cta_rows<CG>() + epi_half * 128 +
+                             quad * 32;
+        const int nch = bn / 32;
+        auto process = [&](uint32_t (&r)[32], int c) {
+          int col0 = nb * bn + c * 32;
+          if (col0 >= N) return;
+          if (glu) {
+            if (!(c & 1)) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float g = __uint_as_float(r[j]);
+                gate[j] = ep.kind == KRR_EPI_GLU_GELU ? gelu_fast(g) : silu(g);
+              }
+              return;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(gate[j] * __uint_as_float(r[j]));
+            col0 = (col0 - 32) / 2;
+          }
+          if (ep.kind != KRR_EPI_QKV_ROPE) {
+            epi_direct<T>(ep, r, row0, lane, col0);
+          } else {
+            __syncwarp();
+            epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, stg);
+          }
+        };
+        uint32_t ra[32], rb[32];
+        tmem_ld32_nowait(tb, ra);
+#pragma unroll 1
+        for (int c = 0; c < nch; c += 2) {
+          tmem_ld_wait();
+          if (c + 1 < nch) tmem_ld32_nowait(tb + (c + 1) * 32, rb);
+          process(ra, c);
+          tmem_ld_wait();
+          if (c + 2 < nch) tmem_ld32_nowait(tb + (c + 2) * 32, ra);
+          if (c + 1 < nch) process(rb, c + 1);
+        }
+      } else {
 #pragma unroll 1
       for (int cc = 0; cc < bn / 32; ++cc) {
         const int h = epi_half, c = cc;
@@ -467,18 +509,13 @@ __global__ void __launch_bounds__(threads<CG>(), 1)
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(gate[j] * __uint_as_float(r[j]));
           col0 = (col0 - 32) / 2;
         }
-        if constexpr (CG == 5) {
-          if (ep.kind != KRR_EPI_QKV_ROPE) {
-            epi_direct<T>(ep, r, row0, lane, col0);
-            continue;
-          }
-        }
-        uint8_t* buf = stg + (CG == 5 ? 0 : (nchunk & 1) * STG_BUF);
+        uint8_t* buf = stg + (nchunk & 1) * STG_BUF;
         ++nchunk;
         // the bulk op that last read this buffer (two chunks ago) must be done
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
         epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, buf);
+      }
       }
       tc_fence_before();
       __syncwarp();

@@ -519,11 +519,9 @@ static int launch(const AttnParams& a, cudaStream_t s) {
            static_cast<const char*>(a.cur_pool), cur_page, a.prefix_valid_len, a.tok_valid,
            a.out, a.kv_heads, a.group, a.seq_len, a.prefix_len, a.layer, a.cur_layer, R,
            pairs, items};
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_fa_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Sm::TOTAL);
-    attr = true;
+  {
+    const int rc = ensure_func_smem((const void*)attn_fa_kernel<T, HD>, Sm::TOTAL);
+    if (rc) return rc;
   }
   const int grid = std::min(items, device_sm_count());
   attn_fa_kernel<T, HD><<<grid, THREADS, Sm::TOTAL, s>>>(mq, mp, mc, p);

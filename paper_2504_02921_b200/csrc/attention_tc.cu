@@ -433,13 +433,9 @@ static int launch(const AttnParams& a, cudaStream_t s) {
            static_cast<const char*>(a.cur_pool), cur_page, a.prefix_valid_len, a.tok_valid,
            a.out, a.kv_heads, a.group, a.seq_len, a.prefix_len, a.layer, a.cur_layer, R,
            row_tiles};
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_tc_kernel<T, HD, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Sm::TOTAL);
-    cudaFuncSetAttribute(attn_tc_kernel<T, HD, KB>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr = true;
+  {
+    const int rc = ensure_func_smem((const void*)attn_tc_kernel<T, HD, KB>, Sm::TOTAL, 100);
+    if (rc) return rc;
   }
   attn_tc_kernel<T, HD, KB><<<(unsigned)(units * row_tiles), THREADS, Sm::TOTAL, s>>>(mq, mp, mc, p);
   return check_launch("attention_tc");

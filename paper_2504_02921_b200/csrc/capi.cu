@@ -2,6 +2,7 @@
 // layer-loop driver krr_forward.
 #include <math_constants.h>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 #include "launchers.h"
@@ -24,15 +25,57 @@ int check_launch(const char* what) {
   return KRR_OK;
 }
 
-int device_sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+static std::mutex g_dev_mu;
+static std::map<std::pair<int, const void*>, int> g_dev_cache;
+
+int cached_per_device(const void* key, int (*compute)(const void*), const void* ctx) {
+  const auto k = std::make_pair(current_device(), key);
+  {
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    auto it = g_dev_cache.find(k);
+    if (it != g_dev_cache.end()) return it->second;
   }
-  return n;
+  const int v = compute(ctx);          // outside the lock: may call into the runtime
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  return g_dev_cache.emplace(k, v).first->second;
+}
+
+static int sm_count_of(const void*) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
+  return n > 0 ? n : 148;
+}
+
+int device_sm_count() {
+  static const char key = 0;
+  return cached_per_device(&key, sm_count_of, nullptr);
+}
+
+struct SmemReq { const void* func; int bytes, carveout; };
+static int apply_smem(const void* ctx) {
+  const SmemReq* r = static_cast<const SmemReq*>(ctx);
+  cudaError_t e = cudaFuncSetAttribute(r->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       r->bytes);
+  if (e == cudaSuccess && r->carveout >= 0)
+    e = cudaFuncSetAttribute(r->func, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             r->carveout);
+  return e == cudaSuccess ? r->bytes : -(int)e;
+}
+
+int ensure_func_smem(const void* func, int smem_bytes, int carveout) {
+  SmemReq r{func, smem_bytes, carveout};
+  // keyed by the function (+1: other per-device values keyed by the same kernel
+  // use the plain pointer); a kernel's smem size is a compile-time constant
+  const int v = cached_per_device(static_cast<const char*>(func) + 1, apply_smem, &r);
+  if (v < 0) return fail(KRR_ECUDA, std::string("cudaFuncSetAttribute failed: ") +
+                                        cudaGetErrorString((cudaError_t)(-v)));
+  return KRR_OK;
 }
 
 // ---------------------------------------------------------------- profiling
@@ -243,6 +286,57 @@ __global__ void topk_kernel(const float* __restrict__ scores, const int32_t* __r
   }
 }
 
+// Long segments: bitonic sort of (score desc, doc id asc, index asc) keys in
+// shared memory (seg_len padded to a power of two, up to 16384 = 192 KB).
+__device__ __forceinline__ uint32_t score_desc_key(float v) {
+  uint32_t u = __float_as_uint(v == 0.f ? 0.f : v);          // -0 == +0
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);           // ascending in v
+  return ~u;                                                 // descending in v
+}
+
+__global__ void topk_bitonic_kernel(const float* __restrict__ scores,
+                                    const int32_t* __restrict__ ids, int seg_len, int n2, int k,
+                                    int32_t* __restrict__ out_idx, float* __restrict__ out_score) {
+  extern __shared__ uint8_t sm[];
+  uint64_t* key = reinterpret_cast<uint64_t*>(sm);            // (score key << 32) | (id ^ sign)
+  int32_t* pos = reinterpret_cast<int32_t*>(key + n2);
+  const int seg = blockIdx.x;
+  const float* sc = scores + (int64_t)seg * seg_len;
+  const int32_t* id = ids + (int64_t)seg * seg_len;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (i < seg_len) {
+      key[i] = ((uint64_t)score_desc_key(sc[i]) << 32) | (uint32_t)(id[i] ^ INT32_MIN);
+      pos[i] = i;
+    } else {
+      key[i] = ~0ull;
+      pos[i] = INT32_MAX;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (n2 >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = key[lo], b = key[hi];
+        const int32_t pa = pos[lo], pb = pos[hi];
+        const bool gt = a > b || (a == b && pa > pb);
+        if (gt == up) {
+          key[lo] = b; key[hi] = a;
+          pos[lo] = pb; pos[hi] = pa;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = threadIdx.x; r < k; r += blockDim.x) {
+    const bool ok = r < seg_len;
+    out_idx[(int64_t)seg * k + r] = ok ? pos[r] : -1;
+    if (out_score) out_score[(int64_t)seg * k + r] = ok ? sc[pos[r]] : -CUDART_INF_F;
+  }
+}
+
 // codec.py:82-95 / 98-115: code * scale[kvh][c]; INT4 low nibble first, sign-extended.
 template <typename T>
 __global__ void dequant_kernel(const uint8_t* __restrict__ codes, const float* __restrict__ scales,
@@ -411,17 +505,9 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
   }
   ProfScope ps(s, 1);
   if (backend == KRR_ATTN_TCGEN05) {
-    // KRR_ATTN_TC_KERNEL = fa (default: P in TMEM) | pp (P via smem) | v1 (one tile/CTA);
-    // A/B switch, fixed per process.  head_dim 256 always uses the one-tile
-    // kernel (its O accumulator needs 256 TMEM columns).
-    static int which = -1;
-    if (which < 0) {
-      const char* e = getenv("KRR_ATTN_TC_KERNEL");
-      which = !e ? 0 : (!strcmp(e, "pp") ? 1 : !strcmp(e, "v1") ? 2 : !strcmp(e, "fa2") ? 3 : 0);
-    }
-    if (which == 2 || p.head_dim == 256) return launch_attention_tcgen05(act, p, s);
-    if (which == 1) return launch_attention_pingpong(act, p, s);
-    if (which == 3) return launch_attention_fa2(act, p, s);
+    // head_dim 256 (Gemma shape) uses the one-tile kernel: its O accumulator
+    // needs 256 TMEM columns, leaving no room for a second tile's S/P
+    if (p.head_dim == 256) return launch_attention_tcgen05(act, p, s);
     return launch_attention_fa(act, p, s);
   }
   if (backend == KRR_ATTN_MMA) return launch_attention_mma(act, p, s);
@@ -574,10 +660,21 @@ int krr_segmented_topk(const float* scores, const int32_t* doc_ids, int32_t n_se
   KRR_REQUIRE(seg_len >= 0 && seg_len <= 16384, KRR_ESHAPE, "top-k segment too long");
   KRR_REQUIRE(k >= 1, KRR_ECONFIG, "top-k needs k >= 1");
   if (n_seg == 0) return KRR_OK;
-  const size_t smem = (size_t)seg_len * 8;
-  topk_kernel<<<n_seg, 256, smem, (cudaStream_t)stream>>>(scores, doc_ids, seg_len, k, out_idx,
-                                                          out_score);
-  return check_launch("segmented_topk");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (seg_len <= 2048) {
+    // rank by counting: O(n^2 / threads), 8 B of smem per candidate (<= 16 KB)
+    const size_t smem = (size_t)seg_len * 8;
+    topk_kernel<<<n_seg, 256, smem, s>>>(scores, doc_ids, seg_len, k, out_idx, out_score);
+    return check_launch("segmented_topk");
+  }
+  int n2 = 1;
+  while (n2 < seg_len) n2 <<= 1;
+  const int smem = n2 * 12;                                  // <= 192 KB at 16384
+  const int rc = ensure_func_smem((const void*)topk_bitonic_kernel, 16384 * 12);
+  if (rc) return rc;
+  topk_bitonic_kernel<<<n_seg, 1024, smem, s>>>(scores, doc_ids, seg_len, n2, k, out_idx,
+                                                out_score);
+  return check_launch("segmented_topk_bitonic");
 }
 
 int krr_dequant_kv(const uint8_t* codes, const float* scales, int32_t bits, int32_t kv_heads,

@@ -22,6 +22,15 @@ std::atomic<uint64_t>& launch_counter();
 // Checks the launch that was just queued; counts it.
 int check_launch(const char* what);
 
+// Per-device, thread-safe launch setup (a process may drive several GPUs from
+// several threads): SM count of the current device; the dynamic-smem opt-in
+// (and carveout, when >= 0) of a kernel applied once per (device, kernel);
+// an int computed once per (device, key) -- e.g. co-resident cluster counts.
+int current_device();
+int device_sm_count();
+int ensure_func_smem(const void* func, int smem_bytes, int carveout = -1);
+int cached_per_device(const void* key, int (*compute)(const void* ctx), const void* ctx);
+
 #define KRR_REQUIRE(cond, code, msg)            \
   do {                                          \
     if (!(cond)) return ::krr::fail(code, msg); \

@@ -41,6 +41,10 @@
 #include "epilogue.cuh"
 #include "tc_ptx.cuh"
 
+#ifndef KRR_TMA_HINT
+#define KRR_TMA_HINT 0
+#endif
+
 namespace krr {
 namespace tc {
 
@@ -353,6 +357,11 @@ __global__ void __launch_bounds__(threads<CG>(), 1)
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
+#if KRR_TMA_HINT == 1
+    const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+#elif KRR_TMA_HINT == 2
+    const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_normal();
+#endif
     for (int tile = cid; tile < tiles; tile += ncl) {
       int mb, nb;
       tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
@@ -364,20 +373,34 @@ __global__ void __launch_bounds__(threads<CG>(), 1)
             const int b_rows = bn / CS;                 // this CTA's slice of the weight tile
             mbar_expect_tx(&full[stage], C::A_BYTES + bn * BK * 2);
             const uint32_t bar = smem_u32(&full[stage]);
+#if KRR_TMA_HINT
+            tma_load_hint<1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
+                             mb * C::TILE_M + (int)rank * cta_rows<CG>(), pol_a);
+            tma_load_mc_hint(sB + stage * C::B_BYTES + rank * (b_rows * BK * 2), &tmB, bar,
+                             kb * BK, nb * bn + (int)rank * b_rows, MC_MASK, pol_b);
+#else
             tma_load<1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
                         mb * C::TILE_M + (int)rank * cta_rows<CG>());
             tma_load_mc(sB + stage * C::B_BYTES + rank * (b_rows * BK * 2), &tmB, bar,
                         kb * BK, nb * bn + (int)rank * b_rows, MC_MASK);
+#endif
           } else {
             // all TMA bytes of the pair land on the leader's barrier
             const uint32_t bar = CG == 2 ? mapa_rank(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
             if (leader)
               mbar_expect_tx(&full[stage], CG == 2 ? 2 * (C::A_BYTES + C::B_BYTES)
                                                    : C::A_BYTES + bn * BK * 2);
+#if KRR_TMA_HINT
+            tma_load_hint<CG == 2 ? 2 : 1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
+                                           mb * C::TILE_M + (int)rank * 128, pol_a);
+            tma_load_hint<CG == 2 ? 2 : 1>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
+                                           nb * bn + (int)rank * C::B_ROWS, pol_b);
+#else
             tma_load<CG>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
                          mb * C::TILE_M + (int)rank * 128);
             tma_load<CG>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
                          nb * bn + (int)rank * C::B_ROWS);
+#endif
           }
         }
         __syncwarp();
@@ -596,10 +619,9 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
     if (raster == 1 || (raster == 2 && cost_n < 0.7 * cost_m)) group_m = -gn;
   }
   constexpr int SMEM = smem_bytes<CG>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tcgen05_kernel<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
+  {
+    const int rc = ensure_func_smem((const void*)gemm_tcgen05_kernel<T, CG>, SMEM);
+    if (rc) return rc;
   }
   const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + bn - 1) / bn);
   constexpr int CS = cluster_size<CG>();
@@ -615,18 +637,20 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   // persistent grid: as many clusters as can be co-resident (GPC boundaries
-  // can leave SMs unusable for larger clusters), queried once per shape class
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
-    cfg.gridDim = dim3((device_sm_count() / CS) * CS);
-    int n = 0;
-    if (CS > 1 && cudaOccupancyMaxActiveClusters(&n, gemm_tcgen05_kernel<T, CG>, &cfg) == cudaSuccess &&
-        n > 0)
-      max_clusters = n;
-    else
-      max_clusters = device_sm_count() / CS;
-    cudaGetLastError();
-  }
+  // can leave SMs unusable for larger clusters), queried once per device
+  const int max_clusters = cached_per_device(
+      (const void*)gemm_tcgen05_kernel<T, CG>,
+      [](const void* c) -> int {
+        cudaLaunchConfig_t q = *static_cast<const cudaLaunchConfig_t*>(c);
+        q.gridDim = dim3((device_sm_count() / CS) * CS);
+        int n = 0;
+        if (CS > 1 && cudaOccupancyMaxActiveClusters(&n, gemm_tcgen05_kernel<T, CG>, &q) ==
+                          cudaSuccess && n > 0)
+          return n;
+        cudaGetLastError();
+        return device_sm_count() / CS;
+      },
+      &cfg);
   const int grid = std::min(CS * tiles, CS * max_clusters);
   cfg.gridDim = dim3(grid);
   cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, CG>, ma, mb, mo, M, N, K, idesc, group_m, bn, ep);

@@ -35,9 +35,7 @@ struct AttnParams {
 };
 int launch_attention_mma(int act_dtype, const AttnParams& p, cudaStream_t s);
 int launch_attention_tcgen05(int act_dtype, const AttnParams& p, cudaStream_t s);
-int launch_attention_pingpong(int act_dtype, const AttnParams& p, cudaStream_t s);
 int launch_attention_fa(int act_dtype, const AttnParams& p, cudaStream_t s);
-int launch_attention_fa2(int act_dtype, const AttnParams& p, cudaStream_t s);
 bool attention_tcgen05_supported(int act_dtype, const AttnParams& p);
 int attention_tcgen05_occupancy(int act_dtype, int head_dim, int* out);
 int launch_attention_simt(int act_dtype, const AttnParams& p, cudaStream_t s);

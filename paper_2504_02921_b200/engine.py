@@ -88,7 +88,7 @@ def _extent(t):
 def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
                 prefix_valid, prefix_ptrs, cur_ptrs, cur_kv_layers: int, last_index=None,
                 scores=None, stream=None, prefix_pool=None, cur_pool=None, x_in=None,
-                x_out=None) -> None:
+                x_out=None, ws: "_Workspace | None" = None) -> None:
     """One krr_forward call over n sequences (all device tensors, contiguous):
     tokens int32 [n, T], tok_valid uint8 [n, T], prefix_valid int32 [n],
     prefix_ptrs / cur_ptrs int64 [n], last_index int32 [n], scores f32 [n].
@@ -100,7 +100,7 @@ def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
         return
     rows = n * T
     need = workspace_bytes(w, rows)
-    ws = _workspace(w.device).get(need, w.device)
+    ws = (ws or _workspace(w.device)).get(need, w.device)
     pp, pb = _extent(prefix_pool)
     cp, cb = _extent(cur_pool)
     b = _lib.Batch(n, T, pos0, prefix_len, cur_kv_layers, _ptr(tokens), _ptr(tok_valid),
@@ -165,15 +165,19 @@ _SCRATCH: dict = {}
 
 
 def score_slots(w: DeviceWeights, pool: KVPool, slots, q_tokens, q_valid=None, last_index=None,
-                max_rows: int | None = None, out=None):
+                max_rows: int | None = None, out=None, ws=None, scratch=None):
     """Score pairs (pool slot, query tokens) on the device; returns f32 [n] on device.
 
-    slots int [n] (host or device), q_tokens int [n, Q] (host or device)."""
+    slots int [n] (host or device), q_tokens int [n, Q] (host or device).
+    ``ws`` / ``scratch``: private workspace / suffix scratch (a CUDA graph's);
+    default the per-device shared ones."""
     with device_lock(w.device):
-        return _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out)
+        return _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, ws,
+                            scratch)
 
 
-def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out):
+def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, ws=None,
+                 scratch=None):
     import torch
     if pool.code != w.code:
         raise ConfigError(f"pool dtype {pool.dtype} != weights dtype {w.dtype}")
@@ -193,7 +197,7 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out):
     prefix_valid = pool.valid_len[slots_t]
     scores = out if out is not None else torch.empty(n, dtype=torch.float32, device=dev)
     step = max(1, (max_rows or rows_budget(w)) // Q)
-    scratch = _SCRATCH.setdefault(str(dev), SuffixScratch())
+    scratch = scratch or _SCRATCH.setdefault(str(dev), SuffixScratch())
     D = pool.document_len
     for i in range(0, n, step):
         j = min(n, i + step)
@@ -201,7 +205,7 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out):
         run_forward(w, q[i:j].contiguous(), q_valid[i:j].contiguous(), D, D,
                     prefix_valid[i:j].contiguous(), prefix_ptrs[i:j].contiguous(), cur, 1,
                     last_index[i:j].contiguous(), scores[i:j], prefix_pool=pool.slab,
-                    cur_pool=scratch.extent())
+                    cur_pool=scratch.extent(), ws=ws)
     return scores
 
 
@@ -350,7 +354,11 @@ class GraphedScorer:
     length Q + per-query top-k) for a fixed batch shape, for latency-critical
     serving: the ~7 launches per layer and the host-side argument marshalling
     are recorded once; a call is two small H2D copies, one graph launch and a
-    D2H of the top-k.  Inputs are copied into static device buffers."""
+    D2H of the top-k.  Inputs are copied into static device buffers.
+
+    The graph owns its workspace and suffix scratch (eager calls cannot
+    reallocate memory it replays into), replays under the device lock, and is
+    re-captured when the pool's slab was re-homed (``KVPool.grow``)."""
 
     def __init__(self, w: DeviceWeights, pool: KVPool, n_q: int, n_c: int, Q: int, k: int):
         import torch
@@ -362,7 +370,15 @@ class GraphedScorer:
         self.ids = torch.arange(n, dtype=torch.int32, device=dev)
         self.qidx = torch.arange(n_q, device=dev).repeat_interleave(n_c)
         self.scores = torch.empty(n, dtype=torch.float32, device=dev)
+        self._ws = _Workspace()
+        self._scratch = SuffixScratch()
         self.stream = torch.cuda.Stream(device=dev)
+        with device_lock(dev):
+            self._capture()
+
+    def _capture(self):
+        import torch
+        dev = self.w.device
         self.stream.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(self.stream):
             for _ in range(2):                    # warm-up: workspace, descriptors, attributes
@@ -372,10 +388,13 @@ class GraphedScorer:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, stream=self.stream):
             self.out_idx, self.out_sc = self._body()
+        self._generation = self.pool.generation
+        self._slab_ptr = self.pool.slab.data_ptr()
 
     def _body(self):
         score_slots(self.w, self.pool, self.slots, self.q.index_select(0, self.qidx),
-                    out=self.scores, max_rows=self.n_q * self.n_c * self.Q)
+                    out=self.scores, max_rows=self.n_q * self.n_c * self.Q, ws=self._ws,
+                    scratch=self._scratch)
         return segmented_topk(self.scores, self.ids, self.n_q, self.n_c, self.k)
 
     def __call__(self, slots, q_tokens, doc_ids):
@@ -383,8 +402,12 @@ class GraphedScorer:
         returns (idx, scores) host arrays [n_q, k] (idx = position within the query's
         candidates)."""
         import torch
-        self.slots.copy_(torch.as_tensor(np.asarray(slots, np.int64)), non_blocking=True)
-        self.q.copy_(torch.as_tensor(np.asarray(q_tokens, np.int32)), non_blocking=True)
-        self.ids.copy_(torch.as_tensor(np.asarray(doc_ids, np.int32)), non_blocking=True)
-        self.graph.replay()
-        return self.out_idx.cpu().numpy(), self.out_sc.cpu().numpy()
+        with device_lock(self.w.device):
+            if (self.pool.generation != self._generation or
+                    self.pool.slab.data_ptr() != self._slab_ptr):
+                self._capture()
+            self.slots.copy_(torch.as_tensor(np.asarray(slots, np.int64)), non_blocking=True)
+            self.q.copy_(torch.as_tensor(np.asarray(q_tokens, np.int32)), non_blocking=True)
+            self.ids.copy_(torch.as_tensor(np.asarray(doc_ids, np.int32)), non_blocking=True)
+            self.graph.replay()
+            return self.out_idx.cpu().numpy(), self.out_sc.cpu().numpy()

@@ -52,14 +52,31 @@ class KVPool:
         self._by_id: dict[str, int] = {}
         self._id_of: dict[int, str] = {}
         self._free = list(range(capacity - 1, -1, -1))
+        self._owned: set[int] = set()
         self._lock = threading.Lock()
+        self.generation = 0
 
-    def grow(self, capacity: int) -> None:
-        """Re-home the slab with more slots (slot ids and handles stay valid)."""
+    def grow(self, capacity: int, min_capacity: int | None = None) -> None:
+        """Re-home the slab with more slots (slot ids and handles stay valid).
+
+        The copy needs old + new slab at once, so the target is clamped to what
+        the device can hold (keeping 1 GiB of headroom); below ``min_capacity``
+        (default: ``capacity``) it fails with StoreError instead of driving the
+        device out of memory.  Pointers into the old slab (CUDA graphs, cached
+        pointer tables) are invalidated; ``generation`` counts re-homes."""
         import torch
         with self._lock:
             if capacity <= self.capacity:
                 return
+            need = capacity if min_capacity is None else max(min_capacity, self.capacity + 1)
+            free, _ = torch.cuda.mem_get_info(self.device)
+            fits = self.capacity + max(0, (free - (1 << 30)) // self.slot_bytes)
+            if fits < need:
+                raise StoreError(
+                    f"KV pool full ({self.capacity} slots of {self.slot_bytes} B); growing to "
+                    f"{need} slots needs {(need - self.capacity) * self.slot_bytes >> 20} MiB "
+                    f"more than the {free >> 20} MiB free on {self.device}")
+            capacity = int(min(capacity, fits))
             slab = torch.empty((capacity, *self.page_shape), dtype=self.slab.dtype,
                                device=self.device)
             slab[:self.capacity].copy_(self.slab)
@@ -70,10 +87,16 @@ class KVPool:
             self._free = list(range(capacity - 1, self.capacity - 1, -1)) + self._free
             self.slab, self.valid_len, self._valid_host = slab, vl, hv
             self.capacity = capacity
+            self.generation += 1
+
+    @property
+    def free_slots(self) -> int:
+        return len(self._free)
 
     # ---------------------------------------------------------- page table
     def __len__(self) -> int:
-        return len(self._by_id)
+        """Slots in use: page-table entries plus caller-owned slots."""
+        return len(self._by_id) + len(self._owned)
 
     def __contains__(self, chunk_id: str) -> bool:
         return chunk_id in self._by_id
@@ -99,6 +122,33 @@ class KVPool:
             if slot is not None:
                 self._id_of.pop(slot, None)
                 self._free.append(slot)
+
+    def allocate_owned(self, n: int) -> np.ndarray:
+        """n slots outside the page table, owned by the caller (e.g. a
+        DeviceKV lease) and returned with ``free_owned``."""
+        with self._lock:
+            if len(self._free) < n:
+                raise StoreError(f"KV pool full ({self.capacity} slots)")
+            out = np.array([self._free.pop() for _ in range(n)], dtype=np.int64)
+            self._owned.update(int(s) for s in out)
+            return out
+
+    def free_owned(self, slots) -> None:
+        with self._lock:
+            for s in np.atleast_1d(np.asarray(slots, dtype=np.int64)):
+                s = int(s)
+                if s in self._owned:
+                    self._owned.discard(s)
+                    self._free.append(s)
+
+    @property
+    def entries(self) -> int:
+        """Page-table entries (keyed slots)."""
+        return len(self._by_id)
+
+    @property
+    def owned(self) -> int:
+        return len(self._owned)
 
     def lookup(self, chunk_ids) -> np.ndarray:
         """chunk ids -> slots (-1 for a miss)."""
@@ -256,7 +306,8 @@ class HostKVTier:
         return np.array([self._by_id.get(c, -1) for c in chunk_ids], dtype=np.int64)
 
     def __len__(self) -> int:
-        return len(self._by_id)
+        """Slots in use: page-table entries plus caller-owned slots."""
+        return len(self._by_id) + len(self._owned)
 
     def __contains__(self, chunk_id: str) -> bool:
         return chunk_id in self._by_id

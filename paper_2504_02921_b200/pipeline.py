@@ -23,7 +23,7 @@ from . import engine
 from .errors import ConfigError, ShapeError
 from .kvpool import KVPool
 from .model import RerankModel
-from .reranker import ScoredPair, _doc_valid
+from .reranker import ScoredPair, _check_vocab, _doc_valid
 
 
 @dataclass
@@ -67,6 +67,9 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
     if any((row != 0).sum() == 0 for row in q):
         from .errors import DegenerateInputError
         raise DegenerateInputError("query is entirely padding")
+    # the reference's _check_call rejects ids outside [0, vocab) (model.py:203-204);
+    # checked before the int32 cast so int64 ids cannot wrap into range
+    _check_vocab(model, q)
     if len(candidates) != n_q:
         raise ShapeError("one candidate list per query")
     lens = np.array([len(c) for c in candidates], dtype=np.int64)
@@ -91,7 +94,7 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
         for dd in docs:
             _doc_valid(model, dd)
         stage = KVPool(model.config, model.layout.document_len, len(miss), w.dtype, dev)
-        st_slots = stage.allocate([f"__miss_{i}" for i in range(len(miss))])
+        st_slots = stage.allocate_owned(len(miss))
         engine.prefill_slots(w, stage, st_slots, docs, (docs != 0).sum(axis=1))
         qi = torch.as_tensor(pair_q[miss], device=dev)
         scores[torch.as_tensor(miss, device=dev)] = engine.score_slots(
@@ -147,8 +150,10 @@ def populate_store(model: RerankModel, docs, index, store, scheme=None, path: st
             by_pool.setdefault(key, []).append(j)
         for key, js in by_pool.items():
             pool = targets[js[0]].pool if key else None
+            # device shards: pages registered under the doc id in the shard's
+            # pool (the store owns them); bytes shards: a temporary owned page
             kvs = doc_prefill_batch(model, toks[js], [chunk[j].id for j in js], path=path,
-                                    pool=pool)
+                                    pool=pool, register=bool(key))
             for j, kv in zip(js, kvs):
                 d, b = chunk[j], targets[j]
                 if key:
@@ -158,7 +163,7 @@ def populate_store(model: RerankModel, docs, index, store, scheme=None, path: st
                 else:
                     data = encode_entry(kv, scheme)
                     store.put_entry(d.id, index.centroid_of(d.id), data)
-                    kv.kv.pool.release(kv.chunk_id)
+                    kv.kv.lease.release()
                     n = len(data)
                 total += n
                 if on_entry is not None:

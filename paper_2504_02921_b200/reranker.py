@@ -19,7 +19,8 @@ are in where things live and how they run:
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import weakref
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -30,18 +31,37 @@ from .hashing import fnv1a64
 from .kvpool import KVPool
 from .model import KVTensorSet, RerankModel
 
-__all__ = ["DocKV", "DeviceKV", "CounterReport", "ScoredPair", "RerankModel", "LayoutConfig",
+__all__ = ["DocKV", "DeviceKV", "SlotLease", "CounterReport", "ScoredPair", "RerankModel", "LayoutConfig",
            "tokenize", "doc_prefill", "doc_prefill_batch", "score_full", "score_reuse",
            "score_batch", "pool_for"]
 
 
+class SlotLease:
+    """Ownership of one caller-owned KVPool slot: the slot returns to the pool
+    when the last reference to the lease (held by a DeviceKV) goes away, so a
+    reference-style ``doc_prefill`` loop does not grow the pool without bound."""
+
+    __slots__ = ("pool", "slot", "_fin", "__weakref__")
+
+    def __init__(self, pool: KVPool, slot: int):
+        self.pool, self.slot = pool, slot
+        self._fin = weakref.finalize(self, pool.free_owned, [slot])
+
+    def release(self) -> None:
+        self._fin()
+
+
 @dataclass(frozen=True)
 class DeviceKV:
-    """KVTensorSet look-alike for a cache resident in a KVPool slot."""
+    """KVTensorSet look-alike for a cache resident in a KVPool slot.
+
+    ``lease`` is set when the DocKV owns its slot (``doc_prefill``); handles
+    onto page-table entries (a device store's pages) carry none."""
 
     pool: KVPool
     slot: int
     position_offset: int = 0
+    lease: SlotLease | None = field(default=None, compare=False, repr=False)
 
     @property
     def token_count(self) -> int:
@@ -182,7 +202,8 @@ def _check_path(path: str) -> None:
 
 # ------------------------------------------------------------ pools
 def pool_for(model: RerankModel, path: str = "fast", min_free: int = 1) -> KVPool:
-    """The model's default HBM pool for a path's precision (grows on demand)."""
+    """The model's default HBM pool for a path's precision (grows on demand,
+    within the device's free memory)."""
     w = model.weights_for(path)
     pools = model.__dict__.setdefault("_pools", {})
     pool = pools.get(w.dtype)
@@ -190,13 +211,16 @@ def pool_for(model: RerankModel, path: str = "fast", min_free: int = 1) -> KVPoo
         pool = KVPool(model.config, model.layout.document_len, max(64, min_free), w.dtype,
                       w.device)
         pools[w.dtype] = pool
-    free = pool.capacity - len(pool)
-    if free < min_free:
-        pool.grow(max(pool.capacity * 2, len(pool) + min_free))
+    short = min_free - pool.free_slots
+    if short > 0:
+        pool.grow(max(pool.capacity * 2, pool.capacity + short),
+                  min_capacity=pool.capacity + short)
     return pool
 
 
 def _staging_pool(model: RerankModel, path: str, n: int) -> KVPool:
+    """Per-model pool for host DocKVs staged into HBM for one scoring call
+    (used under the device lock; slots are owned by that call)."""
     w = model.weights_for(path)
     st = model.__dict__.setdefault("_staging", {})
     pool = st.get(w.dtype)
@@ -208,9 +232,15 @@ def _staging_pool(model: RerankModel, path: str, n: int) -> KVPool:
 
 # ------------------------------------------------------------ prefill
 def doc_prefill_batch(model: RerankModel, docs_tokens, chunk_ids=None, path: str = "fast",
-                      pool: KVPool | None = None,
-                      counters: CounterReport | None = None) -> list[DocKV]:
-    """Batched doc_prefill: n documents through one device forward into pool pages."""
+                      pool: KVPool | None = None, counters: CounterReport | None = None,
+                      register: bool = False) -> list[DocKV]:
+    """Batched doc_prefill: n documents through one device forward into pool pages.
+
+    By default every DocKV owns a fresh slot (released when the DocKV is
+    dropped), so prefilling the same chunk id twice yields two independent
+    caches, as in the reference.  ``register=True`` instead writes the pages
+    under their chunk ids in the pool's page table (a device store's entries,
+    ``populate_store``); ids must then be non-empty and distinct."""
     _check_path(path)
     docs = np.asarray(docs_tokens)
     if docs.ndim != 2:
@@ -219,23 +249,34 @@ def doc_prefill_batch(model: RerankModel, docs_tokens, chunk_ids=None, path: str
     chunk_ids = list(chunk_ids) if chunk_ids is not None else [""] * n
     if len(chunk_ids) != n:
         raise ShapeError("one chunk id per document")
+    if register and (any(not c for c in chunk_ids) or len(set(chunk_ids)) != n):
+        raise ConfigError("registered prefill needs distinct, non-empty chunk ids")
     valid_lens = np.empty(n, dtype=np.int64)
     for i in range(n):
         _, valid_lens[i] = _doc_valid(model, docs[i])
     w = model.weights_for(path)
     pool = pool if pool is not None else pool_for(model, path, n)
-    anon = [c if c else f"__anon_{id(docs)}_{i}_{np.random.randint(1 << 62)}"
-            for i, c in enumerate(chunk_ids)]
-    slots = pool.allocate(anon)
-    engine.prefill_slots(w, pool, slots, docs, valid_lens)
+    if register:
+        slots = pool.allocate(chunk_ids)
+        leases = [None] * n
+    else:
+        slots = pool.allocate_owned(n)
+        leases = [SlotLease(pool, int(s)) for s in slots]
+    try:
+        engine.prefill_slots(w, pool, slots, docs, valid_lens)
+    except BaseException:
+        for le in leases:
+            if le is not None:
+                le.release()
+        raise
     if counters is not None:
         valid = docs != model.layout.pad_id
         counters.merge(CounterReport(
             linear_token_count=int(valid_lens.sum()),
             attn_mac_pairs=int(pair_count(valid, 0).sum()),
             peak_activation_tokens=int(valid_lens.max()) if n else 0))
-    return [DocKV(chunk_id=c, kv=DeviceKV(pool, int(s)), valid_len=int(v))
-            for c, s, v in zip(chunk_ids, slots, valid_lens)]
+    return [DocKV(chunk_id=c, kv=DeviceKV(pool, int(s), lease=le), valid_len=int(v))
+            for c, s, v, le in zip(chunk_ids, slots, valid_lens, leases)]
 
 
 def doc_prefill(model: RerankModel, doc_tokens, chunk_id: str = "", path: str = "fast",
@@ -271,8 +312,9 @@ def _full_counters(model: RerankModel, doc_tokens: np.ndarray,
 
 def _resolve_kv(model: RerankModel, kvs: list[DocKV], path: str):
     """Group DocKVs by the pool that can serve ``path``; host caches or pools
-    of another precision are staged into a staging pool.  Returns (pool, slots)
-    per group and the group index of each pair."""
+    of another precision are staged into slots of the staging pool owned by
+    this call.  Returns (pool, slots) per group, the group index of each pair,
+    and the staging slots to free.  Caller holds the device lock."""
     w = model.weights_for(path)
     cfg, layout = model.config, model.layout
     expected = (cfg.layers, cfg.kv_heads, layout.document_len, cfg.head_dim)
@@ -282,26 +324,32 @@ def _resolve_kv(model: RerankModel, kvs: list[DocKV], path: str):
              if not (isinstance(d.kv, DeviceKV) and d.kv.pool.code == w.code)]
     staging = _staging_pool(model, path, len(stage)) if stage else None
     st_slots = {}
+    taken = np.zeros(0, np.int64)
     if stage:
-        slots = staging.allocate([f"__stage_{j}" for j in range(len(stage))])
-        for j, i in enumerate(stage):
-            d = kvs[i]
-            host = d.kv.to_host() if isinstance(d.kv, DeviceKV) else d.kv
-            if tuple(host.keys.shape) != expected:
-                raise ShapeError(f"cached KV shape {tuple(host.keys.shape)} does not match "
-                                 f"layout/model {expected}")
-            staging.write_host_kv(int(slots[j]), host.keys, host.values, d.valid_len)
-            st_slots[i] = int(slots[j])
+        taken = staging.allocate_owned(len(stage))
+        try:
+            for j, i in enumerate(stage):
+                d = kvs[i]
+                host = d.kv.to_host() if isinstance(d.kv, DeviceKV) else d.kv
+                if tuple(host.keys.shape) != expected:
+                    raise ShapeError(f"cached KV shape {tuple(host.keys.shape)} does not match "
+                                     f"layout/model {expected}")
+                staging.write_host_kv(int(taken[j]), host.keys, host.values, d.valid_len)
+                st_slots[i] = int(taken[j])
+        except BaseException:
+            staging.free_owned(taken)
+            raise
     for i, d in enumerate(kvs):
         if i in st_slots:
             pool, slot = staging, st_slots[i]
         else:
             pool, slot = d.kv.pool, d.kv.slot
-            pool.set_valid_len([slot], [d.valid_len]) if pool.host_valid_len(slot) != d.valid_len else None
+            if pool.host_valid_len(slot) != d.valid_len:
+                pool.set_valid_len([slot], [d.valid_len])
         g = groups.setdefault(id(pool), (pool, []))
         order.append((id(pool), len(g[1])))
         g[1].append(slot)
-    return groups, order
+    return groups, order, (staging, taken)
 
 
 def _validate_kv(model: RerankModel, doc_kv: DocKV) -> None:
@@ -328,17 +376,20 @@ def score_reuse_many(model: RerankModel, kvs: list[DocKV], queries, path: str = 
         np.zeros((0, model.layout.query_len), bool)
     if not kvs:
         return np.zeros(0, np.float32), []
-    import torch
     w = model.weights_for(path)
-    groups, order = _resolve_kv(model, kvs, path)
-    results = {}
-    for key, (pool, slots) in groups.items():
-        idx = [i for i, (k, _) in enumerate(order) if k == key]
-        sc = engine.score_slots(w, pool, np.asarray(slots), q[idx].astype(np.int32))
-        results[key] = (idx, sc.cpu().numpy())
     out = np.empty(len(kvs), dtype=np.float32)
-    for key, (idx, vals) in results.items():
-        out[idx] = vals
+    # staging + scoring under one device lock: concurrent callers (the
+    # reference's threaded rerank workers) never see each other's staged pages
+    with engine.device_lock(w.device):
+        groups, order, (staging, taken) = _resolve_kv(model, kvs, path)
+        try:
+            for key, (pool, slots) in groups.items():
+                idx = [i for i, (k, _) in enumerate(order) if k == key]
+                sc = engine.score_slots(w, pool, np.asarray(slots), q[idx].astype(np.int32))
+                out[idx] = sc.cpu().numpy()
+        finally:
+            if staging is not None:
+                staging.free_owned(taken)
     dvl = np.array([d.valid_len for d in kvs], dtype=np.int64)
     payload = kvs[0].payload_nbytes
     return out, _reuse_counters(model, dvl, qvalid, payload)
@@ -364,7 +415,7 @@ def score_full_many(model: RerankModel, docs, queries, path: str = "fast"):
     qvalid = np.stack([_query_valid(model, row) for row in q])
     w = model.weights_for(path)
     staging = KVPool(model.config, model.layout.document_len, n, w.dtype, w.device)
-    slots = staging.allocate([f"__full_{i}" for i in range(n)])
+    slots = staging.allocate_owned(n)
     vl = (docs != model.layout.pad_id).sum(axis=1)
     engine.prefill_slots(w, staging, slots, docs, vl)
     sc = engine.score_slots(w, staging, slots, q.astype(np.int32)).cpu().numpy()

@@ -28,7 +28,7 @@ import threading
 from dataclasses import dataclass
 from pathlib import Path
 
-from .errors import StoreError
+from .errors import ShapeError, StoreError
 
 KEY_RE = re.compile(r"^[A-Za-z0-9._\-]+(/[A-Za-z0-9._\-]+)*$")   # store.py:23
 ENTRY_SUFFIX = ".hrkv"
@@ -202,9 +202,18 @@ class DevicePagedKVStore(_Counted):
     def put(self, key: str, value: bytes) -> None:
         from .codec import decode_entry_to_pool, parse_entry
         check_key(key)
-        parse_entry(value)                    # reject bad bytes before taking a slot
+        v = parse_entry(value)                # reject bad bytes before taking a slot
+        L, KVH, D, HD = v.shape
+        if (L, 2, KVH, D, HD) != tuple(self.pool.page_shape):
+            raise ShapeError(f"entry shape {v.shape} does not match pool {self.pool.page_shape}")
+        fresh = key not in self.pool
         slot = int(self.pool.allocate([key])[0])
-        decode_entry_to_pool(value, self.pool, slot)
+        try:
+            decode_entry_to_pool(value, self.pool, slot)
+        except BaseException:
+            if fresh:                           # no half-written page stays mapped
+                self.pool.release(key)
+            raise
         with self._lock:
             self._puts += 1
             self._entry_bytes[key] = len(value)
@@ -227,7 +236,7 @@ class DevicePagedKVStore(_Counted):
         return self.pool.chunk_ids()
 
     def stats(self) -> StoreStats:
-        n = len(self.pool)
+        n = self.pool.entries
         with self._lock:
             return StoreStats(n, n * self.pool.slot_bytes, self._gets, self._puts, self._served)
 

@@ -264,11 +264,21 @@ def test_attention_tcgen05_occupancy_query():
     assert n.value >= 1, n.value
 
 
-def test_segmented_topk():
-    n_seg, seg, k = 5, 100, 20
-    s = torch.randn(n_seg, seg, device="cuda")
-    s[0, 10] = s[0, 20] = s[0, 30] = 5.0   # ties broken by doc id
-    ids = torch.stack([torch.randperm(1000, device="cuda")[:seg] for _ in range(n_seg)]).int()
+@pytest.mark.parametrize("seg,k", [(100, 20), (7, 20), (2048, 20), (3000, 50), (6145, 20),
+                                   (16384, 100)])
+def test_segmented_topk(seg, k):
+    """Rank-by-counting (<= 2048) and the bitonic path (longer segments, which
+    need the smem opt-in): order by (score desc, doc id asc, index asc)."""
+    n_seg = 3
+    g = torch.Generator(device="cuda").manual_seed(seg)
+    s = torch.randn(n_seg, seg, device="cuda", generator=g)
+    s[0, :5] = 5.0                          # ties broken by doc id
+    s[1, :] = torch.round(s[1, :] * 4) / 4  # many ties
+    s[2, -1] = 0.0
+    s[2, 0] = -0.0
+    ids = torch.stack([torch.randperm(4 * seg, device="cuda", generator=g)[:seg]
+                       for _ in range(n_seg)]).int()
+    ids[1, :seg // 2] = ids[1, seg // 2:2 * (seg // 2)]   # duplicate ids: index breaks ties
     idx = torch.empty(n_seg, k, dtype=torch.int32, device="cuda")
     sc = torch.empty(n_seg, k, device="cuda")
     _lib.check(_lib.lib().krr_segmented_topk(s.data_ptr(), ids.data_ptr(), n_seg, seg, k,
@@ -276,8 +286,12 @@ def test_segmented_topk():
     torch.cuda.synchronize()
     s_h, ids_h = s.cpu().numpy(), ids.cpu().numpy()
     for i in range(n_seg):
-        want = sorted(range(seg), key=lambda j: (-s_h[i, j], ids_h[i, j]))[:k]
+        order = np.lexsort((np.arange(seg), ids_h[i], -s_h[i].astype(np.float64)))[:k].tolist()
+        want = order + [-1] * (k - len(order))
         assert idx[i].cpu().tolist() == want
+        got = sc[i].cpu().numpy()
+        assert np.array_equal(got[:len(order)], s_h[i][order])
+        assert np.all(np.isneginf(got[len(order):]))
 
 
 @pytest.mark.parametrize("d", [128, 256, 2048, 4096, 200])

@@ -2,14 +2,18 @@
 """Benchmark: reranked query-doc pairs/s (BASELINE.json metric) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
-    python bench.py --impl reference ...      # the reference CPU path (oracle port)
+    python bench.py --impl reference ...      # the reference's own CPU path (baseline/_ref)
 
 One step = one rerank batch of the configured workload: every (query,
 candidate) pair's query suffix is run on top of the candidate's cached
-document KV (HBM pool), scores go through the per-query top-k, and with N>1
-GPUs each rank scores its own document shard and a NCCL all-gather merges the
-per-rank top-k.  Default workload (N=1): BASELINE configs[2], the
-Mistral-7B-shape reranker, 64 queries x 100 docs x 512 tokens, Q=48.
+document KV (HBM pool), scores go through the per-query top-k.  With N>1 GPUs
+(``--gpus N`` re-launches itself as N ranks under torch.distributed.run) the
+corpus is sharded by document id, rank 0's queries are broadcast, each rank
+scores the pairs whose document it owns, and one NCCL all-gather merges the
+per-rank top-k (strong scaling: the same 6,400 pairs at every N; ``--scaling
+weak`` gives every rank its own corpus and candidate lists).  Default
+workload: BASELINE configs[2], the Mistral-7B-shape reranker, 64 queries x
+100 docs x 512 tokens, Q=48.
 
 Prints ONE JSON line (rank 0).
 """
@@ -126,95 +130,143 @@ class Clocks:
 
 
 # ----------------------------------------------------------------- CPU legs
-def cpu_pairs_per_s(preset, D, Q, budget_s=12.0, max_pairs=8):
-    """Time the oracle port (numpy restatement of the reference forward) on this
-    host.  Small models: whole forward per pair.  7B/Gemma shapes: one layer
-    per pair (weights of that one layer from the reference init), scaled by L."""
-    import oracle
-    from paper_2504_02921_b200.config import PRESETS
-    cfg, lay = PRESETS[preset]
-    ocfg = oracle.OracleConfig(layers=cfg.layers, model_dim=cfg.model_dim, heads=cfg.heads,
-                               kv_heads=cfg.kv_heads, head_dim=cfg.head_dim,
-                               vocab_size=cfg.vocab_size, max_position=cfg.max_position,
-                               document_len=D, query_len=Q, mlp=cfg.mlp, ffn_dim=cfg.ffn_dim,
-                               embed_scale=cfg.embed_scale, attn_scale=cfg.attn_scale)
-    rng = np.random.default_rng(3)
-    per_layer = cfg.model_dim >= 1024
-    if per_layer:
-        one = oracle.OracleConfig(**{**ocfg.__dict__, "layers": 1})
-        w = oracle.init_weights(one, with_embedding=False)
-        kvh, hd = cfg.kv_heads, cfg.head_dim
-        past_k = rng.standard_normal((1, kvh, D, hd)).astype(np.float32)
-        past_v = rng.standard_normal((1, kvh, D, hd)).astype(np.float32)
-        x0 = rng.standard_normal((Q, cfg.model_dim)).astype(np.float32)
-        toks = rng.integers(1, cfg.vocab_size, Q)
-        pos = np.arange(D, D + Q)
-        oracle.forward(w, toks, pos, past_k, past_v, None, x_in=x0)  # warm
-        t0, n = time.perf_counter(), 0
-        while n < max_pairs and (time.perf_counter() - t0) < budget_s:
-            oracle.forward(w, toks, pos, past_k, past_v, None, x_in=x0)
-            n += 1
-        t = (time.perf_counter() - t0) / n * cfg.layers
-        sample = f"{n} pairs x 1 of {cfg.layers} layers (D={D}, Q={Q}), time x{cfg.layers}"
-    else:
-        w = oracle.init_weights(ocfg)
-        docs = rng.integers(1, cfg.vocab_size, (max_pairs, D))
-        q = rng.integers(1, cfg.vocab_size, Q)
-        kvs = [oracle.doc_prefill(w, d) for d in docs[:2]]
-        oracle.score_reuse(w, *kvs[0], q)
-        t0, n = time.perf_counter(), 0
-        while n < 64 and (time.perf_counter() - t0) < budget_s:
-            oracle.score_reuse(w, *kvs[n % 2], q)
-            n += 1
-        t = (time.perf_counter() - t0) / n
-        sample = f"{n} reuse pairs, full {cfg.layers}-layer forward (D={D}, Q={Q})"
-    cores = len(os.sched_getaffinity(0))
-    return 1.0 / t, {"cores": cores, "kind": "port", "sample": sample,
-                     "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS", f"default ({cores})")}
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _import_reference():
+    """The reference package, installed unmodified into baseline/_ref
+    (DESIGN.md §5); None when it is not staged."""
+    if not os.path.isdir(os.path.join(REF_DIR, "kvrerank")):
+        return None
+    sys.path.insert(0, REF_DIR)
+    try:
+        from kvrerank import model, reranker
+        return model, reranker
+    except Exception:
+        return None
+    finally:
+        sys.path.remove(REF_DIR)
+
+
+class RefCPU:
+    """The reference's own CPU path, kvrerank.reranker.score_batch(mode="reuse",
+    path="fast") (reranker.py:265-290), on this host's cores (OpenBLAS default
+    threads).  Shapes with model_dim >= 1024 run ONE of the L layers (the
+    reference's init of a whole 7B model takes ~245 s / 26 GB) and scale the
+    time by L; small shapes run the whole model.  Falls back to the oracle port
+    (kind "port") if baseline/_ref is not staged."""
+
+    def __init__(self, preset, pairs=4):
+        from paper_2504_02921_b200.config import PRESETS
+        cfg, lay = PRESETS[preset]
+        self.L, self.D, self.Q, self.pairs = cfg.layers, lay.document_len, lay.query_len, pairs
+        self.per_layer = cfg.model_dim >= 1024
+        ref = _import_reference()
+        self.kind = "reference" if ref is not None and cfg.mlp == "gelu" else "port"
+        rng = np.random.default_rng(3)
+        docs = rng.integers(1, cfg.vocab_size, (2, self.D))
+        q = rng.integers(1, cfg.vocab_size, self.Q)
+        layers = 1 if self.per_layer else cfg.layers
+        if self.kind == "reference":
+            model, reranker = ref
+            rc = model.ModelConfig(layers=layers, model_dim=cfg.model_dim, heads=cfg.heads,
+                                   kv_heads=cfg.kv_heads, head_dim=cfg.head_dim,
+                                   vocab_size=cfg.vocab_size, max_position=cfg.max_position,
+                                   seed=cfg.seed)
+            rm = reranker.RerankModel.build(rc, reranker.LayoutConfig(document_len=self.D,
+                                                                      query_len=self.Q))
+            kvs = [reranker.doc_prefill(rm, d, chunk_id=f"doc-{i}") for i, d in enumerate(docs)]
+            batch = [("q0", kvs[i % 2].chunk_id, kvs[i % 2], q) for i in range(pairs)]
+            self._run = lambda: reranker.score_batch(rm, batch, mode="reuse", path="fast")
+        else:
+            import oracle
+            ocfg = oracle.OracleConfig(layers=layers, model_dim=cfg.model_dim, heads=cfg.heads,
+                                       kv_heads=cfg.kv_heads, head_dim=cfg.head_dim,
+                                       vocab_size=cfg.vocab_size, max_position=cfg.max_position,
+                                       document_len=self.D, query_len=self.Q, mlp=cfg.mlp,
+                                       ffn_dim=cfg.ffn_dim, embed_scale=cfg.embed_scale,
+                                       attn_scale=cfg.attn_scale)
+            w = oracle.init_weights(ocfg, lazy_embedding=True)
+            kvs = [oracle.doc_prefill(w, d) for d in docs]
+            self._run = lambda: [oracle.score_reuse(w, *kvs[i % 2], q) for i in range(pairs)]
+        self._run()                                    # warm (BLAS threads, caches)
+        self.cores = len(os.sched_getaffinity(0))
+
+    def step(self):
+        """One bounded sample: ``pairs`` pairs (x 1 layer for wide shapes).
+        Returns (wall seconds of the sample, pairs/s of the full model)."""
+        t0 = time.perf_counter()
+        self._run()
+        dt = time.perf_counter() - t0
+        scale = self.L if self.per_layer else 1
+        return dt, self.pairs / (dt * scale)
+
+    def info(self):
+        what = ("kvrerank.reranker.score_batch(mode='reuse', path='fast') from baseline/_ref"
+                if self.kind == "reference" else "oracle port (numpy restatement)")
+        lay = f"1 of {self.L} layers, time x{self.L}" if self.per_layer else f"all {self.L} layers"
+        return {"cores": self.cores, "kind": self.kind,
+                "sample": f"{self.pairs} reuse pairs per step, {lay} (D={self.D}, Q={self.Q}); "
+                          f"{what}",
+                "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS",
+                                               f"default ({self.cores})")}
+
+
+def cpu_pairs_per_s(preset, D, Q, reps=3, pairs=4):
+    """The reference CPU baseline beside the GPU arm (same sampler as --impl reference)."""
+    r = RefCPU(preset, pairs)
+    vals = [r.step()[1] for _ in range(reps)]
+    return float(np.median(vals)), r.info()
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (oracle port), rank 0 only."""
+    """--impl reference: the reference's own CPU path, rank 0 only (other ranks
+    exit without work).  Each step is one bounded sample (RefCPU.step)."""
     if rank != 0:
         return
     preset, corpus, nq, nc, keep = CONFIGS[args.config]
     from paper_2504_02921_b200.config import PRESETS
     cfg, lay = PRESETS[preset]
-    D, Q = lay.document_len, lay.query_len
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        v, info = cpu_pairs_per_s(preset, D, Q, budget_s=4.0, max_pairs=2)
-        if i >= args.warmup:
-            vals.append(v)
+    r = RefCPU(preset, pairs=4)
+    for _ in range(args.warmup):
+        r.step()
+    walls, vals = [], []
+    for _ in range(args.steps):
+        dt, v = r.step()
+        walls.append(dt)
+        vals.append(v)
     value = float(np.median(vals))
+    info = r.info()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * nq * nc * args.gpus / value, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(args, cfg, lay, corpus, nq, nc, keep),
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.mean(walls)), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, cfg, lay, corpus, nq, nc, keep, world),
         "cpu_baseline": {"value": value, "unit": "pairs/s", **info},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "step_definition": "one bounded CPU sample (see cpu_baseline.sample); value = pairs "
+                           "of the full model per second, ms_per_step = wall time of the sample",
     }
     print(json.dumps(line))
 
 
-def workload_config(args, cfg, lay, corpus, nq, nc, keep):
-    strong = getattr(args, "scaling", "weak") == "strong"
-    n_cand = nc if strong else nc * args.gpus
-    where = (f"one {corpus}-doc corpus sharded by doc id over {args.gpus} GPU(s)" if strong
-             else f"corpus {corpus} docs/GPU HBM-resident")
+def workload_config(args, cfg, lay, corpus, nq, nc, keep, world):
+    strong = getattr(args, "scaling", "strong") == "strong"
+    n_cand = nc if strong else nc * world
+    where = (f"one {corpus}-doc corpus sharded by doc id over {world} GPU(s)" if strong
+             else f"corpus {corpus} docs/GPU HBM-resident, {world} GPU(s)")
     return {"workload": f"{CONFIGS[args.config][0]}: {nq} queries x {n_cand} docs x "
                         f"{lay.document_len} tok, query suffix {lay.query_len}, {where}",
             "scaling_mode": "strong" if strong else "weak",
             "layers": cfg.layers, "model_dim": cfg.model_dim, "heads": cfg.heads,
             "kv_heads": cfg.kv_heads, "head_dim": cfg.head_dim, "mlp": "gelu_tanh 4d",
             "queries": nq, "candidates_per_query": n_cand, "doc_len": lay.document_len,
-            "query_len": lay.query_len, "corpus_docs_per_gpu": corpus, "keep": keep,
-            "parallelism": f"doc-shard x{args.gpus} + NCCL all-gather top-k"
-            if args.gpus > 1 else "1 GPU",
+            "query_len": lay.query_len,
+            "corpus_docs": corpus if strong else corpus * world, "keep": keep,
+            "parallelism": (f"doc-shard x{world}: queries broadcast, local top-k, one NCCL "
+                            f"all-gather merge" if world > 1 else "1 GPU"),
             "l2": "inputs larger than L2 (KV pool + weights >> 126 MB), no flush"}
 
 
@@ -385,10 +437,15 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     prefill_s = time.perf_counter() - t0
 
-    # ---- queries (broadcast: same on every rank) and per-rank candidates
-    qrng = np.random.default_rng(7)
-    q_host = qrng.integers(1, cfg.vocab_size, (nq, Q), dtype=np.int64)
-    q_dev = torch.as_tensor(q_host.astype(np.int32), device=dev)
+    # ---- queries: generated on rank 0 and broadcast (north_star (d)); per-rank candidates
+    bdev = dev if world == 1 or dist.get_backend() == "nccl" else torch.device("cpu")
+
+    def bcast(qh):
+        return shard.broadcast_queries(qh if rank == 0 else None, nq, Q, device=bdev)
+    q_host = np.random.default_rng(7).integers(1, cfg.vocab_size, (nq, Q), dtype=np.int64) \
+        if rank == 0 else None
+    q_dev = bcast(q_host).to(dev)
+    q_host = q_dev.cpu().numpy().astype(np.int64)
     k = min(keep, nc)
     if strong:
         crng = np.random.default_rng(100)
@@ -458,9 +515,12 @@ def run_ours(args, rank, world, local_rank):
     pairs_step = nq * nc * (1 if strong else world)
     value = pairs_step * args.steps / (ms / 1e3)
 
-    # ---- e2e through the public API (host inputs -> host top-k), max over ranks
+    # ---- e2e through the public API (host inputs -> host top-k), max over ranks:
+    # rank 0's host query tokens are broadcast, every rank reranks its shard
+    # through pipeline.rerank, and the per-rank top-k are merged
     def e2e_step():
-        res = pipeline.rerank(model, pool, [f"q{i}" for i in range(nq)], q_host, cand_ids, k)
+        qh = bcast(q_host).cpu().numpy() if world > 1 else q_host
+        res = pipeline.rerank(model, pool, [f"q{i}" for i in range(nq)], qh, cand_ids, k)
         if world > 1:       # pad ragged local top-k lists to k before the merge
             sc = torch.tensor([[p.score for p in r] + [float("-inf")] * (k - len(r))
                                for r in res.selected], device=dev)
@@ -553,7 +613,7 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic (reference random-init weights, seed 0; "
                                               "uniform token ids)",
-            "config": workload_config(args, cfg, lay, corpus, nq, nc, keep),
+            "config": workload_config(args, cfg, lay, corpus, nq, nc, keep, world),
             "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "paper_2504_02921_b200.pipeline.rerank"},
             "gpu_launches": int(launches),
@@ -589,13 +649,30 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
+def relaunch(n: int) -> int:
+    """``python bench.py --gpus N`` without a launcher: run this same command as
+    N ranks (one per GPU) under torch.distributed.run on 127.0.0.1, with NCCL's
+    init log on so the communicator's rank count is visible on stderr."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every GPU its own corpus shard and candidate lists (default); "
-                         "strong: one corpus sharded by doc id, the same candidates split "
-                         "across GPUs (SURVEY §8(d) protocol)")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default, SURVEY §8(d) protocol): one corpus sharded by doc "
+                         "id, the same queries and candidate lists split across GPUs; "
+                         "weak: every GPU its own corpus shard and candidate lists")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -613,7 +690,13 @@ def main():
     ap.add_argument("--host-quant", default="", choices=["", "int8", "int4"],
                     help="C5: keep host-tier pages HRKV-quantised (2x/4x fewer PCIe bytes)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     # test hook: run every rank on one device (e.g. a 2-rank gloo check of the

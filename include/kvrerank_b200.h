@@ -85,6 +85,9 @@ typedef struct {
   const float* rope_sin;
   void* q_out;
   void* const* kv_seq;     /* device array [n_seqs] of KV slab pointers */
+  /* device [n_seqs*seq_len] absolute RoPE positions (model.py:358 takes any
+   * strictly increasing positions), or NULL: row r sits at pos0 + r % seq_len */
+  const int32_t* positions;
 } krr_qkv_t;
 
 /* Model: per-layer weights are K-major ([out, in]) in act dtype (f32/f16/bf16). */
@@ -137,6 +140,9 @@ typedef struct {
    * layer (before the final norm) is copied there and every layer runs in full. */
   const float* x_in;
   float* x_out;
+  /* device [n_seqs*seq_len] absolute positions (RoPE), or NULL = pos0 + t;
+   * the caller checks them against max_position */
+  const int32_t* positions;
 } krr_batch_t;
 
 const char* krr_last_error(void);

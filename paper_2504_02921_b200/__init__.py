@@ -13,6 +13,7 @@ from .codec import (QuantScheme, decode_entry, decode_entry_to_pool, dequantize_
 from .config import PRESETS, LayoutConfig, ModelConfig
 from .errors import (CodecError, ConfigError, DegenerateInputError, DuplicateChunkError,
                      FormatError, KvRerankError, PositionError, ShapeError, StoreError)
+from .forward import forward, forward_fn
 from .kvpool import HostKVTier, KVPool
 from .model import KVTensorSet, RerankModel
 from .reranker import (CounterReport, DeviceKV, DocKV, ScoredPair, doc_prefill,

@@ -38,7 +38,7 @@ i32, i64, u64 = C.c_int32, C.c_int64, C.c_uint64
 class QKV(C.Structure):
     _fields_ = [("heads", i32), ("kv_heads", i32), ("head_dim", i32), ("seq_len", i32),
                 ("pos0", i32), ("layer", i32), ("kv_len", i32), ("rope_cos", vp),
-                ("rope_sin", vp), ("q_out", vp), ("kv_seq", vp)]
+                ("rope_sin", vp), ("q_out", vp), ("kv_seq", vp), ("positions", vp)]
 
 
 class Model(C.Structure):
@@ -56,7 +56,7 @@ class Batch(C.Structure):
                 ("cur_kv_layers", i32), ("tokens", vp), ("tok_valid", vp), ("prefix_valid_len", vp),
                 ("prefix_kv", vp), ("cur_kv", vp), ("last_index", vp), ("scores", vp),
                 ("prefix_pool", vp), ("prefix_pool_bytes", i64), ("cur_pool", vp),
-                ("cur_pool_bytes", i64), ("x_in", vp), ("x_out", vp)]
+                ("cur_pool_bytes", i64), ("x_in", vp), ("x_out", vp), ("positions", vp)]
 
 
 _LIB = None

@@ -780,7 +780,8 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
   const int n_up = gated ? 2 * F : F;                 // up-projection GEMM width
   const int64_t rows = (int64_t)b->n_seqs * b->seq_len;
   if (rows == 0) return KRR_OK;
-  KRR_REQUIRE(b->pos0 + b->seq_len <= m->max_position, KRR_ESHAPE, "positions exceed max_position");
+  KRR_REQUIRE(b->positions || b->pos0 + b->seq_len <= m->max_position, KRR_ESHAPE,
+              "positions exceed max_position");
   KRR_REQUIRE(b->cur_kv_layers == 1 || b->cur_kv_layers == L, KRR_ECONFIG,
               "cur_kv_layers must be 1 or layers");
   size_t need = 0;
@@ -820,7 +821,7 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     ep.N = nqkv;
     const int cl = b->cur_kv_layers == 1 ? 0 : l;
     ep.qkv = krr_qkv_t{H, KVH, HD, b->seq_len, b->pos0, cl, b->seq_len,
-                       m->rope_cos, m->rope_sin, qb, b->cur_kv};
+                       m->rope_cos, m->rope_sin, qb, b->cur_kv, b->positions};
     rc = do_gemm(m->gemm_backend, act, xn, m->wqkv[l], rows, nqkv, d, ep, s);
     if (rc) return rc;
     // Prefill needs only K/V from the last layer: the rest of that layer

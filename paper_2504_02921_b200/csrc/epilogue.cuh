@@ -69,7 +69,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& ep, int64_t row, int 
   const int G = H / KVH;
   const int64_t b = row / SL;
   const int t = (int)(row - b * SL);
-  const int pos = q.pos0 + t;
+  const int pos = q.positions ? q.positions[row] : q.pos0 + t;
   const float* cs = q.rope_cos + (int64_t)pos * (HD / 2);
   const float* sn = q.rope_sin + (int64_t)pos * (HD / 2);
   for (int j = 0; j < n; j += 2) {

@@ -201,8 +201,9 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap
   const int c0 = col0 - head * q.head_dim;
   if (head < q.heads + q.kv_heads) {
     const int64_t my_row = row0 + lane;
-    const int t = (int)(my_row % q.seq_len);
-    const int64_t off = (int64_t)(q.pos0 + t) * (q.head_dim / 2) + (c0 >> 1);
+    const int pos = q.positions ? (my_row < M ? q.positions[my_row] : 0)
+                                : q.pos0 + (int)(my_row % q.seq_len);
+    const int64_t off = (int64_t)pos * (q.head_dim / 2) + (c0 >> 1);
     const float4* cp = reinterpret_cast<const float4*>(q.rope_cos + off);
     const float4* sp = reinterpret_cast<const float4*>(q.rope_sin + off);
 #pragma unroll

@@ -88,7 +88,7 @@ def _extent(t):
 def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
                 prefix_valid, prefix_ptrs, cur_ptrs, cur_kv_layers: int, last_index=None,
                 scores=None, stream=None, prefix_pool=None, cur_pool=None, x_in=None,
-                x_out=None, ws: "_Workspace | None" = None) -> None:
+                x_out=None, ws: "_Workspace | None" = None, positions=None) -> None:
     """One krr_forward call over n sequences (all device tensors, contiguous):
     tokens int32 [n, T], tok_valid uint8 [n, T], prefix_valid int32 [n],
     prefix_ptrs / cur_ptrs int64 [n], last_index int32 [n], scores f32 [n].
@@ -105,7 +105,7 @@ def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
     cp, cb = _extent(cur_pool)
     b = _lib.Batch(n, T, pos0, prefix_len, cur_kv_layers, _ptr(tokens), _ptr(tok_valid),
                    _ptr(prefix_valid), _ptr(prefix_ptrs), _ptr(cur_ptrs), _ptr(last_index),
-                   _ptr(scores), pp, pb, cp, cb, _ptr(x_in), _ptr(x_out))
+                   _ptr(scores), pp, pb, cp, cb, _ptr(x_in), _ptr(x_out), _ptr(positions))
     if stream is None:
         stream = torch.cuda.current_stream(w.device).cuda_stream
     _lib.check(_lib.lib().krr_forward(C.byref(w.struct()), C.byref(b), ws.data_ptr(),

@@ -24,6 +24,31 @@ import numpy as np
 PAD_ID = np.iinfo(np.int32).max
 
 
+def broadcast_queries(q_tokens, n_q: int, query_len: int, device=None, src: int = 0,
+                      group=None):
+    """Queries are broadcast (north_star (d)): rank ``src`` holds the host
+    token matrix ``[n_q, query_len]``; every rank returns it as an int32 tensor
+    on ``device`` (its GPU for NCCL; the CPU for gloo).  Ids are range-checked
+    as int64 on the source before the int32 cast."""
+    import torch
+    import torch.distributed as dist
+    if device is None:
+        device = torch.device("cpu")
+    rank = dist.get_rank(group) if dist.is_initialized() else src
+    if rank == src:
+        q = np.asarray(q_tokens, dtype=np.int64)
+        if q.shape != (n_q, query_len):
+            raise ValueError(f"query tokens must be [{n_q}, {query_len}], got {q.shape}")
+        if q.size and (q.min() < 0 or q.max() > np.iinfo(np.int32).max):
+            raise ValueError("query token ids outside int32")
+        t = torch.as_tensor(q.astype(np.int32)).to(device)
+    else:
+        t = torch.empty((n_q, query_len), dtype=torch.int32, device=device)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.broadcast(t, src=src, group=group)
+    return t
+
+
 def owner_of(doc_index, world: int):
     """Rank that holds a document's KV (contiguous-free, load-balanced)."""
     return np.asarray(doc_index) % world

@@ -199,14 +199,103 @@ def codec_fixture(model, reranker):
     np.savez_compressed(os.path.join(HERE, "codec_c1.npz"), **out)
 
 
+def c5_fixture(model, reranker, L=2):
+    """C5 geometry at 7B width, L layers: D=2048 docs
+    (positions up to 2047+Q, max_position 4096), Q in {16, 48, 256}, padded
+    docs and queries.  One prefill per doc (the DocKV depends on D only), then
+    every doc x query pair through the reference's score_batch per Q."""
+    cfg = model.ModelConfig(layers=L, model_dim=4096, heads=32, kv_heads=8, head_dim=128,
+                            vocab_size=32000, max_position=4096, seed=0)
+    t0 = time.time()
+    w = model.init_weights(cfg)
+    head = reranker._score_head(cfg)
+    t_init = time.time() - t0
+    D = 2048
+    rng = np.random.default_rng(2048)
+    docs = _tokens(rng, 4, D, cfg.vocab_size)
+    docs[1, D - 300:] = 0
+    docs[2, 1000:] = 0
+    rm = reranker.RerankModel(config=cfg, weights=w, score_head=head,
+                              layout=reranker.LayoutConfig(document_len=D, query_len=48))
+    t0 = time.time()
+    kvs = [reranker.doc_prefill(rm, d, chunk_id=f"c5-{i}") for i, d in enumerate(docs)]
+    t_pre = time.time() - t0
+    out = {"doc_tokens": docs, "valid_len": np.array([k.valid_len for k in kvs]),
+           "cfg": np.array([cfg.layers, cfg.model_dim, cfg.heads, cfg.kv_heads, cfg.head_dim,
+                            cfg.vocab_size, cfg.max_position]),
+           # K/V of doc 0 at positions 1500..1563 (RoPE beyond 1024), both layers
+           "doc0_keys_1500": np.ascontiguousarray(kvs[0].kv.keys[:, :, 1500:1564]),
+           "doc0_values_1500": np.ascontiguousarray(kvs[0].kv.values[:, :, 1500:1564]),
+           "init_seconds": np.float64(t_init), "prefill_seconds": np.float64(t_pre)}
+    for Q in (16, 48, 256):
+        rmq = reranker.RerankModel(config=cfg, weights=w, score_head=head,
+                                   layout=reranker.LayoutConfig(document_len=D, query_len=Q))
+        qs = _tokens(rng, 2, Q, cfg.vocab_size)
+        qs[1, Q - Q // 4:] = 0                       # trailing pads
+        qs[1, 1] = 0                                 # interior pad
+        pairs = [(f"q{j}", kv.chunk_id, kv, qs[j]) for j in range(2) for kv in kvs]
+        t0 = time.time()
+        scored, counters = reranker.score_batch(rmq, pairs, mode="reuse", path="fast")
+        out[f"q{Q}_tokens"] = qs
+        out[f"q{Q}_scores"] = np.array([p.score for p in scored], np.float64)
+        out[f"q{Q}_seconds"] = np.float64(time.time() - t0)
+        out[f"q{Q}_counters"] = np.array([counters.linear_token_count, counters.attn_mac_pairs,
+                                          counters.peak_activation_tokens,
+                                          counters.kv_bytes_loaded])
+    np.savez_compressed(os.path.join(HERE, f"c5w_l{L}.npz"), **out)
+    print("c5", "init", round(t_init, 1), "prefill", round(t_pre, 1))
+
+
+def topk_fixture(model, reranker, pipeline, name, cfg_kw, D, n_docs, keep, seed):
+    """1 query x n_docs candidates at full width (shallow): the reference's
+    scores and its own _select top-keep (pipeline.py:285-287)."""
+    from types import SimpleNamespace
+    cfg = model.ModelConfig(**cfg_kw)
+    rm = reranker.RerankModel.build(cfg, reranker.LayoutConfig(document_len=D, query_len=48))
+    rng = np.random.default_rng(seed)
+    docs = _tokens(rng, n_docs, D, cfg.vocab_size)
+    docs[5, D - 100:] = 0
+    query = _tokens(rng, 1, 48, cfg.vocab_size)[0]
+    query[44:] = 0
+    t0 = time.time()
+    kvs = [reranker.doc_prefill(rm, d, chunk_id=f"doc-{i:05d}") for i, d in enumerate(docs)]
+    scored, _ = reranker.score_batch(rm, [("q0", kv.chunk_id, kv, query) for kv in kvs],
+                                     mode="reuse", path="fast")
+    sel = pipeline._select(SimpleNamespace(config=SimpleNamespace(keep_m=keep)), scored)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), doc_tokens=docs, query_tokens=query,
+                        scores=np.array([p.score for p in scored], np.float64),
+                        top_ids=np.array([p.chunk_id for p in sel]),
+                        top_scores=np.array([p.score for p in sel], np.float64),
+                        cfg=np.array([cfg.layers, cfg.model_dim, cfg.heads, cfg.kv_heads,
+                                      cfg.head_dim, cfg.vocab_size, cfg.max_position]),
+                        cpu_seconds=np.float64(time.time() - t0))
+    print(name, "scored in", round(time.time() - t0, 1), "s")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-wide", action="store_true")
     ap.add_argument("--only", default="")
     args = ap.parse_args()
     model, reranker = _ref()
+    from kvrerank import pipeline
+    only = {
+        "codec": lambda: codec_fixture(model, reranker),
+        "c5": lambda: c5_fixture(model, reranker),
+        "topk_c3w": lambda: topk_fixture(
+            model, reranker, pipeline, "topk_c3w_l2",
+            dict(layers=2, model_dim=4096, heads=32, kv_heads=8, head_dim=128,
+                 vocab_size=32000, max_position=1024, seed=0), D=512, n_docs=100, keep=20,
+            seed=21),
+        "topk_c2w": lambda: topk_fixture(
+            model, reranker, pipeline, "topk_c2w_l1",
+            dict(layers=1, model_dim=2048, heads=8, kv_heads=1, head_dim=256,
+                 vocab_size=256000, max_position=1024, seed=0), D=512, n_docs=100, keep=20,
+            seed=22),
+    }
     if args.only:
-        {"codec": lambda: codec_fixture(model, reranker)}[args.only]()
+        for k in args.only.split(","):
+            only[k]()
         return
     codec_fixture(model, reranker)
     weights_fixture(model)
@@ -222,6 +311,8 @@ def main():
                      dict(layers=1, model_dim=2048, heads=8, kv_heads=1, head_dim=256,
                           vocab_size=256000, max_position=1024, seed=0),
                      D=512, Q=48, n_pairs=4, seed=8)
+        for k in ("c5", "topk_c3w", "topk_c2w"):
+            only[k]()
 
 
 if __name__ == "__main__":

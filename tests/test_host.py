@@ -4,6 +4,7 @@ reference-mirroring config/validation logic, counters and the no-fallback rule."
 import ctypes
 import os
 import re
+import sys
 
 import numpy as np
 import pytest
@@ -140,3 +141,13 @@ def test_header_enums_match_host_constants():
             "KRR_ATTN_SIMT": _lib.ATTN_SIMT, "KRR_ATTN_TCGEN05": _lib.ATTN_TCGEN05}
     for name, v in want.items():
         assert vals.get(name) == v, (name, vals.get(name), v)
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    """bench.py --gpus N under a launcher must match WORLD_SIZE (no silent
+    single-process run reporting N GPUs)."""
+    import subprocess
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                       env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr

@@ -167,3 +167,42 @@ def test_variant_oracle_is_self_consistent(variant):
     k, v, vl = oracle.doc_prefill(w, doc)
     assert oracle.score_reuse(w, k, v, vl, q) == pytest.approx(oracle.score_full(w, doc, q),
                                                               rel=1e-5, abs=1e-6)
+
+
+def test_c5_geometry_oracle_vs_reference(golden_dir):
+    """C5 geometry (7B width, L=2, D=2048, RoPE positions past 1,024, Q=16 with
+    padded doc and query): the oracle reproduces the reference's score."""
+    g = np.load(os.path.join(golden_dir, "c5w_l2.npz"))
+    L, d, H, KVH, HD, V, MP = [int(x) for x in g["cfg"]]
+    cfg = oracle.OracleConfig(layers=L, model_dim=d, heads=H, kv_heads=KVH, head_dim=HD,
+                              vocab_size=V, max_position=MP, document_len=2048, query_len=16)
+    w = oracle.init_weights(cfg, lazy_embedding=True)
+    k, v, vl = oracle.doc_prefill(w, g["doc_tokens"][1])            # 300 trailing pads
+    assert vl == g["valid_len"][1]
+    s = oracle.score_reuse(w, k, v, vl, g["q16_tokens"][1])          # padded query
+    r = g["q16_scores"]
+    assert abs(s - r[4 + 1]) <= 1e-4 * max(abs(r[5]), np.sqrt(np.mean(r ** 2)))
+
+
+@pytest.mark.parametrize("name", ["topk_c3w_l2", "topk_c2w_l1"])
+def test_topk_goldens_follow_select_order(golden_dir, name):
+    """The reference's _select output (pipeline.py:285-287) is the oracle's
+    (score desc, chunk id asc) order over the 100 golden scores."""
+    g = np.load(os.path.join(golden_dir, f"{name}.npz"))
+    ids = [f"doc-{i:05d}" for i in range(len(g["scores"]))]
+    order = oracle.select_topk(list(g["scores"]), ids, 20)
+    assert [ids[i] for i in order] == list(g["top_ids"])
+    assert np.array_equal(g["scores"][order], g["top_scores"])
+
+
+def test_topk_c2w_oracle_scores(golden_dir):
+    """Two of the 100 Gemma-width candidates (one padded) re-scored by the oracle."""
+    g = np.load(os.path.join(golden_dir, "topk_c2w_l1.npz"))
+    L, d, H, KVH, HD, V, MP = [int(x) for x in g["cfg"]]
+    cfg = oracle.OracleConfig(layers=L, model_dim=d, heads=H, kv_heads=KVH, head_dim=HD,
+                              vocab_size=V, max_position=MP, document_len=512, query_len=48)
+    w = oracle.init_weights(cfg, lazy_embedding=True)
+    r = g["scores"]
+    s = np.array([oracle.score_full(w, g["doc_tokens"][i], g["query_tokens"]) for i in (0, 5)])
+    rms = np.sqrt(np.mean(r ** 2))
+    assert np.all(np.abs(s - r[[0, 5]]) <= 1e-4 * np.maximum(np.abs(r[[0, 5]]), rms))

@@ -106,3 +106,32 @@ def test_local_work_partition_covers_every_pair_once():
             pos = np.sort(w.seg_pos[w.pair_query == qi])
             assert pos.tolist() == list(range(pos.size)) and pos.size <= w.seg_len
     assert (seen == 1).all()
+
+
+def _bcast_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        toks = np.arange(3 * 7, dtype=np.int64).reshape(3, 7) + 100 if rank == 0 else None
+        t = shard.broadcast_queries(toks, 3, 7)
+        q.put((rank, t.dtype == torch.int32, t.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_broadcast_queries(world):
+    """Rank 0's query tokens reach every rank unchanged (north_star (d))."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = (np.arange(21).reshape(3, 7) + 100).tolist()
+    assert sorted(r for r, _, _ in res) == list(range(world))
+    assert all(ok and got == want for _, ok, got in res)

@@ -9,19 +9,22 @@
 //                             in TMEM (2 x 256 columns, double buffered)
 //   warps 2..5  epilogue:     tcgen05.ld 32x32b.x32 -> fused epilogue -> TMA store
 //
-// Tile shapes share the code (template CG):
-//   CG=1  128x256 tile per CTA, cta_group::1, 4-stage ring of 48 KB
-//   CG=2  256x256 tile per CTA pair (cluster of 2), cta_group::2: CTA r loads
-//         rows [r*128, r*128+128) of both the A and the B tile (32 KB per
-//         stage, 6 stages); the leader issues the MMAs, commits are multicast
-//         to both CTAs, both epilogues release the accumulator on the leader.
-//   CG=3  (default) 128x256 per CTA with cta_group::1 MMAs, clusters of 2
-//         M-adjacent CTAs: each loads its A tile and HALF of the shared weight
-//         tile, multicast into both CTAs (TMA .multicast::cluster); a stage is
-//         recycled when both CTAs' MMAs committed (multicast tcgen05.commit).
-//         L2->SM traffic per k-block 32 KB instead of 48 KB; on the power-capped
-//         B200 that is worth ~6% higher clocks (profiles/).
-//   CG=4  as CG=3 with clusters of 4 (slower; kept for A/B).
+// Every CTA owns 128 output rows x one 256-wide (or narrower) N tile; the
+// geometries differ in how the weight tile reaches the tensor cores:
+//   G=1  single CTA, cta_group::1 M=128 MMAs; the CTA loads its whole B tile.
+//   G=3  cluster of 2 M-adjacent CTAs, cta_group::1 MMAs; each CTA TMA-loads
+//        half of B and multicasts it into both CTAs.  L2->SM 32 KB per CTA and
+//        k-block, 48 KB written into each CTA's smem and read by its MMAs.
+//   G=7  (default for large M) cluster of 4 = two CTA pairs on M-adjacent
+//        256-row tiles sharing the weight tile.  Each pair runs cta_group::2
+//        M=256 MMAs issued by its leader: every SM holds only ITS half of B
+//        (the pair MMA reads both halves), and that half arrives as two 64-row
+//        pieces, one loaded by this CTA and one by the same-half CTA of the
+//        other pair, each multicast into both.  Per CTA and k-block: 24 KB read
+//        from L2, 32 KB written into smem, 32 KB of operands read by the
+//        tensor cores (G=3: 32 / 48 / 48) -- operand movement is what the
+//        power cap charges for (profiles/r02_gemm_geometry.txt).
+//   G=2  one CTA pair (cluster of 2) without the cross-pair multicast (A/B).
 //
 // Epilogues: RESIDUAL adds the accumulator into the f32 residual stream with a
 // TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add, the read-modify-write
@@ -30,8 +33,8 @@
 // with coalesced 16 B stores.  Staging tiles are 128B/64B-swizzled to match
 // the tensor maps (bank-conflict free) and double buffered per warp.
 //
-// The fixed K order per output tile (no split-K) and a single tile shape for
-// every M keep each row's result independent of batch composition
+// The fixed K order per output tile (no split-K) keeps each row's result
+// independent of batch composition and of the geometry chosen for a launch
 // (SPEC.md:178 batch invariance).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -41,8 +44,10 @@
 #include "epilogue.cuh"
 #include "tc_ptx.cuh"
 
-#ifndef KRR_TMA_HINT
-#define KRR_TMA_HINT 0
+// A/B switch for the pair geometries: 1 = plain TMA per CTA + a relayed
+// "stage landed" arrive to the pair leader instead of cta_group::2 TMA.
+#ifndef KRR_PAIR_RELAY
+#define KRR_PAIR_RELAY 0
 #endif
 
 namespace krr {
@@ -50,59 +55,32 @@ namespace tc {
 
 constexpr int BN = 256, BK = 64;
 constexpr int THREADS = 192;
-// CG=5 drains a single-buffered 256x256 accumulator: 8 epilogue warps (two per
-// TMEM lane quadrant, one per 128-row half) halve the exposed epilogue
-template <int CG> constexpr int threads() { return CG == 5 ? 320 : THREADS; }
-template <int CG> constexpr int epi_warps() { return CG == 5 ? 8 : 4; }
 constexpr int STG_BUF = 4096;                 // one 32x32 chunk (f32) per buffer
 constexpr int STG_WARP_BYTES = 2 * STG_BUF;   // double buffered per epilogue warp
 
-template <int CG> struct Cfg;
-template <> struct Cfg<1> {
-  static constexpr int TILE_M = 128, STAGES = 4, GROUP_M = 16;
-  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 256 * BK * 2;
-  static constexpr int B_ROWS = 256;
+template <int G> struct Geo;
+template <> struct Geo<1> {
+  static constexpr int CS = 1, MMA_CG = 1, STAGES = 4, GROUP_M = 16;
+  static constexpr int B_ROWS_SMEM = 256;     // rows of the weight tile held per CTA
 };
-template <> struct Cfg<2> {
-  static constexpr int TILE_M = 256, STAGES = 6, GROUP_M = 8;
-  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 128 * BK * 2;
-  static constexpr int B_ROWS = 128;
+template <> struct Geo<3> {
+  static constexpr int CS = 2, MMA_CG = 1, STAGES = 4, GROUP_M = 8;
+  static constexpr int B_ROWS_SMEM = 256;
 };
-// CG=3: cta_group::1 MMAs (128x256 per CTA) in a cluster of 2 M-adjacent CTAs
-// that share the weight tile: each CTA TMA-loads half of B (128 rows) and
-// multicasts it to both, so L2->SM traffic per tile drops from 48 to 32 KB
-// per k-block while every MMA still reads only local shared memory.
-template <> struct Cfg<3> {
-  static constexpr int TILE_M = 256, STAGES = 4, GROUP_M = 8;
-  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 256 * BK * 2;
-  static constexpr int B_ROWS = 128;
+template <> struct Geo<2> {
+  static constexpr int CS = 2, MMA_CG = 2, STAGES = 6, GROUP_M = 8;
+  static constexpr int B_ROWS_SMEM = 128;
 };
-// CG=4: as CG=3 with clusters of 4 (each CTA loads a quarter of B): 24 KB of
-// L2->SM traffic per k-block instead of 48.
-template <> struct Cfg<4> {
-  static constexpr int TILE_M = 512, STAGES = 4, GROUP_M = 4;
-  static constexpr int A_BYTES = 128 * BK * 2, B_BYTES = 256 * BK * 2;
-  static constexpr int B_ROWS = 64;
+template <> struct Geo<7> {
+  static constexpr int CS = 4, MMA_CG = 2, STAGES = 6, GROUP_M = 4;
+  static constexpr int B_ROWS_SMEM = 128;
 };
-// CG=5: as CG=3 but each CTA owns 256 rows (two M=128 MMAs per k-step share
-// one B stage, into TMEM columns 0-255 and 256-511): per CTA and k-block
-// 32 KB of A + 32 KB of B for 8.4 MFLOP instead of 48 KB per 4.2 MFLOP, at the
-// price of a single-buffered accumulator (the epilogue of a tile is not
-// overlapped with the next tile's main loop).
-template <> struct Cfg<5> {
-  static constexpr int TILE_M = 512, STAGES = 3, GROUP_M = 4;
-  static constexpr int A_BYTES = 256 * BK * 2, B_BYTES = 256 * BK * 2;
-  static constexpr int B_ROWS = 128;
-};
-// CTAs per cluster: 1 (CG=1), 2 (cta_group::2 pair, or B multicast), 4 (B multicast)
-template <int CG> constexpr int cluster_size() { return CG == 1 ? 1 : CG == 4 ? 4 : 2; }
-// rows of A per CTA (two M=128 MMAs per k-step for CG=5)
-template <int CG> constexpr int cta_rows() { return CG == 5 ? 256 : 128; }
-template <int CG> constexpr bool multicast_b() { return CG >= 3; }
-template <int CG>
-constexpr int smem_bytes() {
-  return Cfg<CG>::STAGES * (Cfg<CG>::A_BYTES + Cfg<CG>::B_BYTES) + 4 * STG_WARP_BYTES +
-         1024 /*align*/ + 512 /*barriers*/;
+constexpr int A_BYTES = 128 * BK * 2;                      // 16 KB: 128 rows per CTA
+template <int G> constexpr int b_bytes() { return Geo<G>::B_ROWS_SMEM * BK * 2; }
+template <int G> constexpr int tile_m() { return 128 * Geo<G>::CS; }   // rows per cluster
+template <int G> constexpr int smem_bytes() {
+  return Geo<G>::STAGES * (A_BYTES + b_bytes<G>()) + 4 * STG_WARP_BYTES + 1024 /*align*/ +
+         512 /*barriers*/;
 }
 
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -117,7 +95,6 @@ __device__ __forceinline__ float gelu_fast(float x) {
   return 0.5f * x * (1.0f + tanh_fast(inner));
 }
 
-template <int CG>
 // Raster: GM > 0 -> groups of GM m-tiles sweep all n-tiles (the activation
 // panels of a group stay in L2); GM < 0 -> bands of -GM n-tiles sweep all
 // m-tiles (a weight band stays in L2 and is read from DRAM once).
@@ -251,79 +228,48 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap
   __syncwarp();
 }
 
-// Direct epilogue (CG=5): no shared-memory staging and no TMA store, so a
-// single-buffered accumulator drains without waiting on bulk-store completion.
-// Thread `lane` owns row row0+lane, columns col0..col0+31 (64 B of 16-bit
-// output or 128 B of f32 residual, contiguous per thread).
-template <typename T>
-__device__ __forceinline__ void epi_direct(const EpiParams& ep, const uint32_t (&r)[32],
-                                           int64_t row0, int lane, int col0) {
-  const int64_t row = row0 + lane;
-  if (row >= ep.M) return;
-  if (ep.kind == KRR_EPI_RESIDUAL) {
-    float4* x = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + row * ep.N + col0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float4 o = x[j];
-      o.x += __uint_as_float(r[4 * j]);
-      o.y += __uint_as_float(r[4 * j + 1]);
-      o.z += __uint_as_float(r[4 * j + 2]);
-      o.w += __uint_as_float(r[4 * j + 3]);
-      x[j] = o;
-    }
-    return;
-  }
-  uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<T*>(ep.out) + row * ep.N + col0);
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-  if (ep.kind == KRR_EPI_GELU) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    o[j] = make_uint4(pack16<T>(v[8 * j], v[8 * j + 1]), pack16<T>(v[8 * j + 2], v[8 * j + 3]),
-                      pack16<T>(v[8 * j + 4], v[8 * j + 5]), pack16<T>(v[8 * j + 6], v[8 * j + 7]));
-}
-
 // ------------------------------------------------------------ kernel
-template <typename T, int CG>
-__global__ void __launch_bounds__(threads<CG>(), 1)
+template <typename T, int G>
+__global__ void __launch_bounds__(THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmOut, int64_t M, int N, int K,
                         uint32_t idesc, int group_m, int bn, EpiParams ep) {
-  using C = Cfg<CG>;
+  using C = Geo<G>;
+  constexpr int CS = C::CS, MMA_CG = C::MMA_CG, STAGES = C::STAGES;
+  constexpr int B_BYTES = b_bytes<G>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
-  uint8_t* stage_base = sB + C::STAGES * C::B_BYTES;
+  uint8_t* sB = sA + STAGES * A_BYTES;
+  uint8_t* stage_base = sB + STAGES * B_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_base + 4 * STG_WARP_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* peer_full = tempty + 2;          // RELAY: peer's stage landed (leader side)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(peer_full + STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr bool CLUSTER = CG >= 2;            // launched as clusters
-  constexpr int MMA_CG = CG == 2 ? 2 : 1;      // cta_group of the MMA / TMEM ops
-  const uint32_t rank = CLUSTER ? cluster_rank() : 0;
-  const bool leader = rank == 0;
+  const uint32_t rank = CS > 1 ? cluster_rank() : 0;
+  // cta_group::2: the pair is (rank & ~1, rank | 1); its even CTA leads
+  const uint32_t pair_leader = MMA_CG == 2 ? (rank & ~1u) : rank;
+  const bool leader = rank == pair_leader;
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    // CG=3: a stage is free only when BOTH CTAs' MMAs have read it (the peer
-    // multicasts its half of B into this CTA's buffer)
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], multicast_b<CG>() ? cluster_size<CG>() : 1);
+      mbar_init(&peer_full[s], 1);
+      // a stage may be refilled once every MMA issuer that reads it committed:
+      // G=3 both CTAs (the peer's B slice lands here), G=7 both pair leaders
+      // (the other pair multicasts a B piece here), else this CTA's (pair's)
+      mbar_init(&empty[s], G == 3 ? 2 : G == 7 ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], epi_warps<CG>() * MMA_CG);
+      mbar_init(&tempty[a], 4 * MMA_CG);    // every epilogue warp of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -341,182 +287,153 @@ __global__ void __launch_bounds__(threads<CG>(), 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CLUSTER) cluster_sync_all();
+  if constexpr (CS > 1) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_m = (int)((M + C::TILE_M - 1) / C::TILE_M);
-  // bn = N-tile width (256, or 128 for narrow layers, CG=1/3 only); the smem
-  // ring and TMEM are sized for 256
+  const int num_m = (int)((M + tile_m<G>() - 1) / tile_m<G>());
   const int num_n = (N + bn - 1) / bn;
   const int tiles = num_m * num_n;
   const int nk = K / BK;
-  constexpr int CS = cluster_size<CG>();
-  constexpr uint16_t MC_MASK = (uint16_t)((1u << CS) - 1);
   const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
 
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
-#if KRR_TMA_HINT == 1
-    const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
-#elif KRR_TMA_HINT == 2
-    const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_normal();
-#endif
     for (int tile = cid; tile < tiles; tile += ncl) {
       int mb, nb;
-      tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
+      tile_coords(tile, num_m, num_n, group_m, mb, nb);
+      const int row_a = mb * tile_m<G>() + (int)rank * 128;
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one_sync()) {
-          if constexpr (multicast_b<CG>()) {
-            // own A rows; own slice of B multicast into every CTA's stage buffer
-            const int b_rows = bn / CS;                 // this CTA's slice of the weight tile
-            mbar_expect_tx(&full[stage], C::A_BYTES + bn * BK * 2);
+          uint8_t* a_dst = sA + stage * A_BYTES;
+          uint8_t* b_dst = sB + stage * B_BYTES;
+          if constexpr (G == 1) {
             const uint32_t bar = smem_u32(&full[stage]);
-#if KRR_TMA_HINT
-            tma_load_hint<1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
-                             mb * C::TILE_M + (int)rank * cta_rows<CG>(), pol_a);
-            tma_load_mc_hint(sB + stage * C::B_BYTES + rank * (b_rows * BK * 2), &tmB, bar,
-                             kb * BK, nb * bn + (int)rank * b_rows, MC_MASK, pol_b);
-#else
-            tma_load<1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
-                        mb * C::TILE_M + (int)rank * cta_rows<CG>());
-            tma_load_mc(sB + stage * C::B_BYTES + rank * (b_rows * BK * 2), &tmB, bar,
-                        kb * BK, nb * bn + (int)rank * b_rows, MC_MASK);
-#endif
+            mbar_expect_tx(&full[stage], A_BYTES + bn * BK * 2);
+            tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
+            tma_load<1>(b_dst, &tmB, bar, kb * BK, nb * bn);
+          } else if constexpr (G == 3) {
+            // own A rows; own slice of B multicast into both CTAs' stage buffers
+            const int b_rows = bn / 2;
+            const uint32_t bar = smem_u32(&full[stage]);
+            mbar_expect_tx(&full[stage], A_BYTES + bn * BK * 2);
+            tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
+            tma_load_mc(b_dst + rank * (b_rows * BK * 2), &tmB, bar, kb * BK,
+                        nb * bn + (int)rank * b_rows, (uint16_t)0x3);
+          } else if constexpr (KRR_PAIR_RELAY) {
+            // pair, relayed: plain TMA into this CTA's own stage and barrier; the
+            // peer's warp 1 forwards "landed" to the leader (peer_full)
+            const uint32_t bar = smem_u32(&full[stage]);
+            mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+            tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
+            const int half = (int)(rank & 1);
+            if constexpr (G == 2) {
+              tma_load<1>(b_dst, &tmB, bar, kb * BK, nb * bn + half * 128);
+            } else {
+              const int p = (int)(rank >> 1);
+              tma_load_mc(b_dst + p * (64 * BK * 2), &tmB, bar, kb * BK,
+                          nb * bn + half * 128 + p * 64, (uint16_t)((1u << rank) | (1u << (rank ^ 2))));
+            }
           } else {
-            // all TMA bytes of the pair land on the leader's barrier
-            const uint32_t bar = CG == 2 ? mapa_rank(smem_u32(&full[stage]), 0) : smem_u32(&full[stage]);
-            if (leader)
-              mbar_expect_tx(&full[stage], CG == 2 ? 2 * (C::A_BYTES + C::B_BYTES)
-                                                   : C::A_BYTES + bn * BK * 2);
-#if KRR_TMA_HINT
-            tma_load_hint<CG == 2 ? 2 : 1>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
-                                           mb * C::TILE_M + (int)rank * 128, pol_a);
-            tma_load_hint<CG == 2 ? 2 : 1>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
-                                           nb * bn + (int)rank * C::B_ROWS, pol_b);
-#else
-            tma_load<CG>(sA + stage * C::A_BYTES, &tmA, bar, kb * BK,
-                         mb * C::TILE_M + (int)rank * 128);
-            tma_load<CG>(sB + stage * C::B_BYTES, &tmB, bar, kb * BK,
-                         nb * bn + (int)rank * C::B_ROWS);
-#endif
+            // pair: every byte of both CTAs' stage lands on the pair leader's barrier
+            const uint32_t bar = mapa_rank(smem_u32(&full[stage]), pair_leader);
+            if (leader) mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+            tma_load<2>(a_dst, &tmA, bar, kb * BK, row_a);
+            const int half = (int)(rank & 1);          // which 128-row half of the N tile
+            if constexpr (G == 2) {
+              tma_load<2>(b_dst, &tmB, bar, kb * BK, nb * bn + half * 128);
+            } else {
+              // piece p (64 rows) of this half, multicast into the same-half CTA of both pairs
+              const int p = (int)(rank >> 1);
+              tma_load_mc2(b_dst + p * (64 * BK * 2), &tmB, bar, kb * BK,
+                           nb * bn + half * 128 + p * 64, (uint16_t)((1u << rank) | (1u << (rank ^ 2))));
+            }
           }
         }
         __syncwarp();
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
     // whole warp walks the schedule; one elected lane issues (descriptors stay
-    // in uniform registers, no per-MMA elect loop)
-    if (CG != 2 || leader) {
+    // in uniform registers); pair geometries: the leader issues for both SMs
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       const uint64_t dA = sw128_desc(smem_u32(sA));
       const uint64_t dB = sw128_desc(smem_u32(sB));
+      // completion of a stage's MMAs frees it in every CTA that holds its operands
+      constexpr uint16_t EMPTY_MASK = G == 3 ? 0x3 : G == 7 ? 0xF : 0x0;
+      const uint16_t pair_mask = (uint16_t)(0x3u << rank);   // (leader, peer)
       for (int tile = cid; tile < tiles; tile += ncl, ++it) {
-        // CG=5 uses both 256-column halves for one tile (rows 0-127 / 128-255)
-        const int acc = CG == 5 ? 0 : (it & 1);
-        const uint32_t acc_phase = CG == 5 ? (it & 1) : ((it >> 1) & 1);
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;   // accumulators 256 columns apart
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
+          if constexpr (MMA_CG == 2 && KRR_PAIR_RELAY) mbar_wait(&peer_full[stage], phase);
           tc_fence_after();
           if (elect_one_sync()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              mma_f16<MMA_CG>(d_tmem, dA + ((stage * C::A_BYTES + k * 32) >> 4),
-                              dB + ((stage * C::B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
-              if constexpr (CG == 5)   // rows 128-255: A + 128 rows x 128 B, TMEM + 256 columns
-                mma_f16<MMA_CG>(d_tmem + BN, dA + ((stage * C::A_BYTES + 128 * 128 + k * 32) >> 4),
-                                dB + ((stage * C::B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
-            }
-            if constexpr (multicast_b<CG>()) mma_commit_mc1(&empty[stage], MC_MASK);
-            else mma_commit<MMA_CG>(&empty[stage]);
+            for (int k = 0; k < BK / 16; ++k)
+              mma_f16<MMA_CG>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
+                              dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+            if constexpr (G == 1) mma_commit<1>(&empty[stage]);
+            else if constexpr (G == 3) mma_commit_mc1(&empty[stage], EMPTY_MASK);
+            else if constexpr (G == 2) mma_commit2_mc(&empty[stage], pair_mask);
+            else mma_commit2_mc(&empty[stage], EMPTY_MASK);
           }
           __syncwarp();
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (elect_one_sync()) mma_commit<MMA_CG>(&tfull[acc]);
+        if (elect_one_sync()) {
+          if constexpr (MMA_CG == 1) mma_commit<1>(&tfull[acc]);
+          else mma_commit2_mc(&tfull[acc], pair_mask);
+        }
         __syncwarp();
       }
+    } else if constexpr (MMA_CG == 2 && KRR_PAIR_RELAY) {
+      // the peer's idle MMA warp relays each landed stage to the leader
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t lead_pf = mapa_rank(smem_u32(&peer_full[0]), pair_leader);
+      for (int tile = cid; tile < tiles; tile += ncl)
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          if (elect_one_sync()) mbar_arrive_cluster(lead_pf + stage * 8);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
     }
   } else {
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    // CG=5: 8 warps share the 4-warp staging area (one 4 KB buffer each; only
-    // the QKV scatter uses it there)
-    uint8_t* stg = stage_base + (warp - 2) * (CG == 5 ? STG_BUF : STG_WARP_BYTES);
-    const int epi_half = CG == 5 ? (warp - 2) >> 2 : 0;   // CG=5: 128-row half this warp drains
-    const uint32_t tempty0 =
-        CG == 2 ? mapa_rank(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+    uint8_t* stg = stage_base + (warp - 2) * STG_WARP_BYTES;
+    const uint32_t tempty0 = MMA_CG == 2 ? mapa_rank(smem_u32(&tempty[0]), pair_leader)
+                                         : smem_u32(&tempty[0]);
     int it = 0, nchunk = 0;
     const bool glu = ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU;
     float gate[32];
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       int mb, nb;
-      tile_coords<CG>(tile, num_m, num_n, group_m, mb, nb);
-      const int acc = CG == 5 ? 0 : (it & 1);
-      const uint32_t acc_phase = CG == 5 ? (it & 1) : ((it >> 1) & 1);
+      tile_coords(tile, num_m, num_n, group_m, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
       // one epilogue warp polls the accumulator barrier; the other three are
       // parked on a named barrier (the poll loop of four warps was ~1/4 of all
       // issued instructions and power)
       if (warp == 2) mbar_wait(&tfull[acc], acc_phase);
-      named_bar_sync(1, 32 * epi_warps<CG>());
+      named_bar_sync(1, 128);
       tc_fence_after();
-      if constexpr (CG == 5) {
-        // this warp's 128-row half: TMEM loads software-pipelined one chunk
-        // ahead of the processing (the single-buffered accumulator's drain is
-        // on the critical path)
-        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (acc + epi_half) * BN;
-        const int64_t row0 = (int64_t)mb * C::TILE_M + rank * cta_rows<CG>() + epi_half * 128 +
-                             quad * 32;
-        const int nch = bn / 32;
-        auto process = [&](uint32_t (&r)[32], int c) {
-          int col0 = nb * bn + c * 32;
-          if (col0 >= N) return;
-          if (glu) {
-            if (!(c & 1)) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const float g = __uint_as_float(r[j]);
-                gate[j] = ep.kind == KRR_EPI_GLU_GELU ? gelu_fast(g) : silu(g);
-              }
-              return;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(gate[j] * __uint_as_float(r[j]));
-            col0 = (col0 - 32) / 2;
-          }
-          if (ep.kind != KRR_EPI_QKV_ROPE) {
-            epi_direct<T>(ep, r, row0, lane, col0);
-          } else {
-            __syncwarp();
-            epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, stg);
-          }
-        };
-        uint32_t ra[32], rb[32];
-        tmem_ld32_nowait(tb, ra);
+      const int64_t row0 = (int64_t)mb * tile_m<G>() + rank * 128 + quad * 32;
 #pragma unroll 1
-        for (int c = 0; c < nch; c += 2) {
-          tmem_ld_wait();
-          if (c + 1 < nch) tmem_ld32_nowait(tb + (c + 1) * 32, rb);
-          process(ra, c);
-          tmem_ld_wait();
-          if (c + 2 < nch) tmem_ld32_nowait(tb + (c + 2) * 32, ra);
-          if (c + 1 < nch) process(rb, c + 1);
-        }
-      } else {
-#pragma unroll 1
-      for (int cc = 0; cc < bn / 32; ++cc) {
-        const int h = epi_half, c = cc;
-        const int64_t row0 = (int64_t)mb * C::TILE_M + rank * cta_rows<CG>() + h * 128 + quad * 32;
+      for (int c = 0; c < bn / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (acc + h) * BN + c * 32, r);
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
         int col0 = nb * bn + c * 32;
         if (col0 >= N) continue;
         if (glu) {
@@ -540,7 +457,6 @@ __global__ void __launch_bounds__(threads<CG>(), 1)
         __syncwarp();
         epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, buf);
       }
-      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
@@ -549,7 +465,7 @@ __global__ void __launch_bounds__(threads<CG>(), 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (CLUSTER) cluster_sync_all();
+  if constexpr (CS > 1) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
     if constexpr (MMA_CG == 1)
@@ -592,42 +508,19 @@ static int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, i
   return KRR_OK;
 }
 
-template <typename T, int CG>
+template <typename T, int G>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int64_t M,
-                  int N, int K, uint32_t idesc, int bn, const EpiParams& ep, cudaStream_t s) {
-  // L2 rasterisation: GROUP_M m-tiles share each weight (B) panel while it is
-  // L2-resident (KRR_GEMM_GROUP_M overrides, fixed per process).
-  static int group_m_env = -1, raster = -1;
-  if (group_m_env < 0) {
-    const char* e = getenv("KRR_GEMM_GROUP_M");
-    group_m_env = (e && atoi(e) > 0) ? atoi(e) : Cfg<CG>::GROUP_M;
-    // m (default) | n | auto: N-bands cut DRAM reads (MLP-up 22.8 -> ~10 GB per
-    // launch) but measured ~1% slower on the power-capped C3 step
-    const char* r = getenv("KRR_GEMM_RASTER");
-    raster = !r ? 0 : (r[0] == 'm' ? 0 : r[0] == 'n' ? 1 : 2);
-  }
-  // DRAM traffic model: M-groups re-read the weight once per group
-  // (|A| + |B|*num_m/GM); N-bands re-read the activations once per band
-  // (|A|*num_n/GN + |B|) with the band (GN x 256 x K x 2 B) held in L2.
-  int group_m = group_m_env;
+                  int N, int K, uint32_t idesc, int bn, int group_m, const EpiParams& ep,
+                  cudaStream_t s) {
+  constexpr int SMEM = smem_bytes<G>();
   {
-    const double A = (double)M * K * 2, B = (double)N * K * 2;
-    const int num_m = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M), num_n = (N + bn - 1) / bn;
-    int gn = (int)((40.0 * (1 << 20)) / (256.0 * K * 2));      // ~40 MB weight band
-    gn = std::max(1, std::min(gn, num_n));
-    const double cost_m = A + B * std::max(1.0, (double)num_m / group_m_env);
-    const double cost_n = A * std::ceil((double)num_n / gn) + B;
-    if (raster == 1 || (raster == 2 && cost_n < 0.7 * cost_m)) group_m = -gn;
-  }
-  constexpr int SMEM = smem_bytes<CG>();
-  {
-    const int rc = ensure_func_smem((const void*)gemm_tcgen05_kernel<T, CG>, SMEM);
+    const int rc = ensure_func_smem((const void*)gemm_tcgen05_kernel<T, G>, SMEM);
     if (rc) return rc;
   }
-  const int tiles = (int)((M + Cfg<CG>::TILE_M - 1) / Cfg<CG>::TILE_M) * ((N + bn - 1) / bn);
-  constexpr int CS = cluster_size<CG>();
+  const int tiles = (int)((M + tile_m<G>() - 1) / tile_m<G>()) * ((N + bn - 1) / bn);
+  constexpr int CS = Geo<G>::CS;
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(threads<CG>());
+  cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];
@@ -640,12 +533,12 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   // persistent grid: as many clusters as can be co-resident (GPC boundaries
   // can leave SMs unusable for larger clusters), queried once per device
   const int max_clusters = cached_per_device(
-      (const void*)gemm_tcgen05_kernel<T, CG>,
+      (const void*)gemm_tcgen05_kernel<T, G>,
       [](const void* c) -> int {
         cudaLaunchConfig_t q = *static_cast<const cudaLaunchConfig_t*>(c);
         q.gridDim = dim3((device_sm_count() / CS) * CS);
         int n = 0;
-        if (CS > 1 && cudaOccupancyMaxActiveClusters(&n, gemm_tcgen05_kernel<T, CG>, &q) ==
+        if (CS > 1 && cudaOccupancyMaxActiveClusters(&n, gemm_tcgen05_kernel<T, G>, &q) ==
                           cudaSuccess && n > 0)
           return n;
         cudaGetLastError();
@@ -654,8 +547,9 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
       &cfg);
   const int grid = std::min(CS * tiles, CS * max_clusters);
   cfg.gridDim = dim3(grid);
-  cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, CG>, ma, mb, mo, M, N, K, idesc, group_m, bn, ep);
-  return check_launch(CG == 2 ? "gemm_tcgen05_2cta" : CG >= 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
+  cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, G>, ma, mb, mo, M, N, K, idesc, group_m, bn, ep);
+  return check_launch(G == 7 ? "gemm_tcgen05_pair_mc" : G == 2 ? "gemm_tcgen05_pair"
+                      : G == 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
 }
 
 }  // namespace tc
@@ -673,55 +567,33 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (ep.kind == KRR_EPI_QKV_ROPE && ep.qkv.head_dim % 32 != 0)
     return launch_gemm_simt(act_dtype, A, B, M, N, K, ep, s);  // a chunk must stay in one head
 
-  // Tile shape (KRR_GEMM_CTA, read once per process):
-  //   1  128x256 per CTA, no cluster
-  //   2  256x256 per CTA pair (cta_group::2)
-  //   3  per-shape 2 / 1
-  //   4  128x256 per CTA, clusters of 2 M-adjacent CTAs sharing the weight tile
-  //      by TMA multicast (DEFAULT: 2/3 of the L2->SM traffic of mode 1; under
-  //      the power cap this buys ~6% higher clocks, +6% pairs/s on C3)
-  //   5  as 4 with clusters of 4 (measured much slower)
-  //   6  as 4 with 256 rows per CTA (Cfg<5>: two MMAs per k-step share one B
-  //      stage); launches with M < 8192 use mode 4
-  static int env_mode = -1;
-  if (env_mode < 0) {
-    const char* e = getenv("KRR_GEMM_CTA");
-    env_mode = e ? atoi(e) : 4;
-    if (env_mode < 1 || env_mode > 6) env_mode = 4;
-  }
-  int mode = env_mode == 3 ? (K <= 4096 && M >= 1024 ? 2 : 1) : env_mode;
-  if (mode == 6 && M < 8192) mode = 4;
-  if (mode == 4 && M <= 128) mode = 1;   // one 128-row tile: a cluster partner would idle
-  const CUtensorMapDataType dt =
-      act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  const int tile_m = mode == 2 ? 256 : 128;
-  // N-tile width (modes 1/4), chosen by a wave model: each candidate width bn
-  // (multiples of 32 so epilogue chunks never straddle a head) gives
-  // units = m-tiles x ceil(N/bn) tiles on `slots` persistent CTAs (clusters),
-  // cost = ceil(units/slots) waves x bn x c(bn), where c(bn) = 1 + 0.3(256/bn - 1)
-  // is the measured per-FLOP penalty of narrower MMAs (A re-read from smem per
-  // N-chunk; profiles/r01_gemm_tile_width_sweep.txt: 1.3x at 128).  Large M
-  // (thousands of waves) always lands on 256; few-wave launches (the
-  // per-query latency batch, C2's N=2048 layers) avoid a mostly-empty last
-  // wave; one-wave launches (host-tier groups) spread the weight stream over
-  // more SMs.  Every width runs the same per-element MMA sequence (full K in
-  // BK-chunk order into one fp32 accumulator), so the choice may depend on M
-  // without breaking batch invariance.  KRR_GEMM_NARROW=0 pins 256.
-  static int narrow = -1;
-  if (narrow < 0) {
-    const char* e = getenv("KRR_GEMM_NARROW");
-    narrow = e ? atoi(e) : 1;
-  }
-  static int force_bn = -1;                 // KRR_GEMM_BN=<multiple of 32, 64..256>: experiments
-  if (force_bn < 0) {
-    const char* e = getenv("KRR_GEMM_BN");
+  // Geometry per launch (KRR_GEMM_GEO overrides for A/B: 1, 2, 3 or 7):
+  //   M <= 128          G=1 (a cluster partner would idle)
+  //   large M           G=7 (pair MMAs + cross-pair weight multicast)
+  //   otherwise         G=3
+  static const int env_geo = [] {
+    const char* e = getenv("KRR_GEMM_GEO");
     const int v = e ? atoi(e) : 0;
-    force_bn = v >= 64 && v <= 256 && v % 32 == 0 ? v : 0;
-  }
+    return (v == 1 || v == 2 || v == 3 || v == 7) ? v : 0;
+  }();
+  int geo = env_geo ? env_geo : (M <= 128 ? 1 : 3);
+  if (geo == 1 && M > 128 && env_geo == 0) geo = 3;
+  // N-tile width for the cta_group::1 geometries, chosen by a wave model: each
+  // candidate width bn (multiples of 32 so epilogue chunks never straddle a
+  // head) gives units = m-tiles x ceil(N/bn) tiles on `slots` persistent
+  // CTAs (clusters), cost = ceil(units/slots) waves x bn x c(bn), where
+  // c(bn) = 1 + 0.3(256/bn - 1) is the measured per-FLOP penalty of narrower
+  // MMAs (A re-read from smem per N-chunk; profiles/r01_gemm_tile_width_sweep.txt:
+  // 1.3x at 128).  Large M (thousands of waves) always lands on 256; few-wave
+  // launches (the per-query latency batch, C2's N=2048 layers) avoid a
+  // mostly-empty last wave.  Every width runs the same per-element MMA
+  // sequence (full K in BK-chunk order into one fp32 accumulator), so the
+  // choice may depend on M without breaking batch invariance.  The pair
+  // geometries keep 256 (their B halves are 128 rows).
   int bn = BN;
-  if (narrow && (mode == 1 || mode == 4)) {
-    const int rows_per_unit = mode == 4 ? 256 : 128;
-    const int64_t slots = mode == 4 ? device_sm_count() / 2 : device_sm_count();
+  if (geo == 1 || geo == 3) {
+    const int rows_per_unit = geo == 3 ? 256 : 128;
+    const int64_t slots = geo == 3 ? device_sm_count() / 2 : device_sm_count();
     const int64_t m_units = (M + rows_per_unit - 1) / rows_per_unit;
     double best = 0;
     for (int cand = 256; cand >= 64; cand -= 32) {
@@ -730,14 +602,20 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
       if (cand == 256 || cost < best * 0.98) { best = cost; bn = cand; }
     }
   }
-  if (force_bn && (mode == 1 || mode == 4)) bn = force_bn;
+  static const int env_gm = [] {
+    const char* e = getenv("KRR_GEMM_GROUP_M");
+    return e ? atoi(e) : 0;
+  }();
+  const int group_m = env_gm > 0 ? env_gm
+                      : geo == 7 ? Geo<7>::GROUP_M : geo == 2 ? Geo<2>::GROUP_M
+                      : geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
+  const CUtensorMapDataType dt =
+      act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap ma, mb, mo;
-  int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, mode == 6 ? 256 : 128,
-                    CU_TENSOR_MAP_SWIZZLE_128B);
+  int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK,
-                mode == 5 ? 64 : mode == 2 ? 128 : (mode == 4 || mode == 6) ? bn / 2 : bn,
-                CU_TENSOR_MAP_SWIZZLE_128B);
+  const uint32_t b_box = geo == 1 ? bn : geo == 3 ? bn / 2 : geo == 2 ? 128 : 64;
+  rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK, b_box, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   if (ep.kind == KRR_EPI_RESIDUAL) {
     KRR_REQUIRE((reinterpret_cast<uintptr_t>(ep.out) & 15) == 0, KRR_ESHAPE, "residual must be 16-byte aligned");
@@ -756,19 +634,19 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (rc) return rc;
   // instruction descriptor: D=f32 @4, A/B f16|bf16 @7/@10, K-major both, N>>3 @17, M>>4 @24
   const uint32_t fmt = act_dtype == KRR_BF16 ? 1u : 0u;
+  const int mma_m = (geo == 2 || geo == 7) ? 256 : 128;
   const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(bn >> 3) << 17) |
-                         ((uint32_t)(tile_m >> 4) << 24);
-  if (act_dtype == KRR_F16)
-    return mode == 2   ? launch<__half, 2>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-           : mode == 6 ? launch<__half, 5>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-           : mode == 4 ? launch<__half, 3>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-           : mode == 5 ? launch<__half, 4>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-                       : launch<__half, 1>(ma, mb, mo, M, N, K, idesc, bn, ep, s);
-  return mode == 2   ? launch<__nv_bfloat16, 2>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-         : mode == 6 ? launch<__nv_bfloat16, 5>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-         : mode == 4 ? launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-         : mode == 5 ? launch<__nv_bfloat16, 4>(ma, mb, mo, M, N, K, idesc, bn, ep, s)
-                     : launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, bn, ep, s);
+                         ((uint32_t)(mma_m >> 4) << 24);
+#define KRR_GEO_LAUNCH(T)                                                             \
+  switch (geo) {                                                                      \
+    case 1: return launch<T, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);      \
+    case 2: return launch<T, 2>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);      \
+    case 7: return launch<T, 7>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);      \
+    default: return launch<T, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);     \
+  }
+  if (act_dtype == KRR_F16) { KRR_GEO_LAUNCH(__half) }
+  KRR_GEO_LAUNCH(__nv_bfloat16)
+#undef KRR_GEO_LAUNCH
 }
 
 }  // namespace krr

@@ -281,6 +281,25 @@ __device__ __forceinline__ void mma_commit_mc1(uint64_t* bar, uint16_t mask) {
       " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// cta_group::2 TMA load multicast to the CTAs in ctaMask; the completion of
+// each destination lands on the mbarrier at `bar`'s offset in the LEADER CTA
+// of that destination's pair (bar = this CTA's barrier address with the peer
+// bit cleared, i.e. a shared::cluster address in the pair leader).
+__device__ __forceinline__ void tma_load_mc2(void* dst, const CUtensorMap* map, uint32_t bar,
+                                             int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+// cta_group::2 MMA completion arriving on the same mbarrier of every CTA in mask.
+__device__ __forceinline__ void mma_commit2_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
 // Named CTA barrier over `count` threads: waiting warps are parked by the
 // hardware (no issue slots, unlike an mbarrier try_wait poll loop).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {

@@ -677,7 +677,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="f16", choices=["f16", "bf16"])
+    # f16 operands (fp32 accumulation): the precision that meets north_star's 2e-2
+    # gate; bf16 misses it on this model (tests/test_gpu_parity_wide.py)
+    ap.add_argument("--precision", default="f16", choices=["f16"])
     ap.add_argument("--corpus", type=int, default=0)
     ap.add_argument("--queries", type=int, default=0)
     ap.add_argument("--cands", type=int, default=0)

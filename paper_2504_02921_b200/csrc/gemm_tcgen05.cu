@@ -606,7 +606,7 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
     const char* e = getenv("KRR_GEMM_GROUP_M");
     return e ? atoi(e) : 0;
   }();
-  const int group_m = env_gm > 0 ? env_gm
+  const int group_m = env_gm != 0 ? env_gm          // < 0: bands of -env_gm n-tiles
                       : geo == 7 ? Geo<7>::GROUP_M : geo == 2 ? Geo<2>::GROUP_M
                       : geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
   const CUtensorMapDataType dt =

@@ -57,15 +57,13 @@ def ref_model(ref):
 
 @pytest.fixture
 def patched(ref, monkeypatch):
-    """The reference's operator switch, rebound the way INTEGRATION.md shows."""
+    """The reference's operator switch with the two paths INTEGRATION.md §2 adds."""
     _, reranker = ref
     orig = reranker._forward_fn
 
     def _forward_fn(path):
-        if path == "fast":
-            return krr.forward_fn("f32")
-        if path == "b200_f16":
-            return krr.forward_fn("f16")
+        if path in ("b200", "b200_f16"):
+            return krr.forward_fn("f32" if path == "b200" else "f16")
         return orig(path)
     monkeypatch.setattr(reranker, "_forward_fn", _forward_fn)
     return reranker
@@ -82,22 +80,23 @@ def test_reference_entry_points_through_b200_forward(patched, ref_model, c1):
     path, DocKVs within 1e-4, counters identical."""
     R = patched
     docs, q = c1["doc_tokens"][:16], c1["query_tokens"]
-    kvs = [R.doc_prefill(ref_model, d, chunk_id=f"doc-{i:05d}") for i, d in enumerate(docs)]
+    kvs = [R.doc_prefill(ref_model, d, chunk_id=f"doc-{i:05d}", path="b200")
+           for i, d in enumerate(docs)]
     k0 = np.asarray(kvs[0].kv.keys)
     assert k0.shape == c1["doc0_keys"].shape
     assert np.max(np.abs(k0 - c1["doc0_keys"])) <= 1e-4 * np.max(np.abs(c1["doc0_keys"]))
     assert np.max(np.abs(np.asarray(kvs[1].kv.values) - c1["doc1_values"])) <= \
         1e-4 * np.max(np.abs(c1["doc1_values"]))
     scored, counters = R.score_batch(ref_model, [("q0", kv.chunk_id, kv, q) for kv in kvs],
-                                     mode="reuse", path="fast")
+                                     mode="reuse", path="b200")
     assert _err([p.score for p in scored], c1["scores_fast"][:16]) <= 1e-4
     # counters are closed-form (reranker.py:293-300): the first 16 of 64 pairs
     want = c1["counters"]
     assert counters.linear_token_count == want[0] // 4
     assert counters.kv_bytes_loaded == want[3] // 4
-    s, _ = R.score_reuse(ref_model, kvs[2], q, path="fast")
+    s, _ = R.score_reuse(ref_model, kvs[2], q, path="b200")
     assert abs(s - c1["scores_fast"][2]) <= 1e-4 * max(1.0, abs(c1["scores_fast"][2]))
-    full = [R.score_full(ref_model, docs[i], q, path="fast")[0] for i in range(2)]
+    full = [R.score_full(ref_model, docs[i], q, path="b200")[0] for i in range(2)]
     assert _err(full, c1["scores_full_fast"][:2]) <= 1e-4
 
 

@@ -606,9 +606,18 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
     const char* e = getenv("KRR_GEMM_GROUP_M");
     return e ? atoi(e) : 0;
   }();
-  const int group_m = env_gm != 0 ? env_gm          // < 0: bands of -env_gm n-tiles
-                      : geo == 7 ? Geo<7>::GROUP_M : geo == 2 ? Geo<2>::GROUP_M
-                      : geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
+  int group_m = env_gm != 0 ? env_gm          // < 0: bands of -env_gm n-tiles
+                : geo == 7 ? Geo<7>::GROUP_M : geo == 2 ? Geo<2>::GROUP_M
+                : geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
+  if (env_gm == 0 && (geo == 2 || geo == 7)) {
+    // pair geometries: keep the weights L2-resident and stream activations --
+    // the whole weight matrix when it fits (QKV, WO: all n-tiles in one band),
+    // else bands of 16 n-tiles when those fit (MLP-up), else M-groups (MLP-down)
+    const double wbytes = (double)N * K * 2;
+    const int num_n = (N + bn - 1) / bn;
+    if (wbytes <= 64.0 * (1 << 20)) group_m = -num_n;
+    else if (16.0 * bn * K * 2 <= 40.0 * (1 << 20)) group_m = -16;
+  }
   const CUtensorMapDataType dt =
       act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap ma, mb, mo;

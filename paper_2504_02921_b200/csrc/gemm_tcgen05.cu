@@ -9,22 +9,17 @@
 //                             in TMEM (2 x 256 columns, double buffered)
 //   warps 2..5  epilogue:     tcgen05.ld 32x32b.x32 -> fused epilogue -> TMA store
 //
-// Every CTA owns 128 output rows x one 256-wide (or narrower) N tile; the
-// geometries differ in how the weight tile reaches the tensor cores:
-//   G=1  single CTA, cta_group::1 M=128 MMAs; the CTA loads its whole B tile.
-//   G=3  cluster of 2 M-adjacent CTAs, cta_group::1 MMAs; each CTA TMA-loads
-//        half of B and multicasts it into both CTAs.  L2->SM 32 KB per CTA and
-//        k-block, 48 KB written into each CTA's smem and read by its MMAs.
-//   G=7  (default for large M) cluster of 4 = two CTA pairs on M-adjacent
-//        256-row tiles sharing the weight tile.  Each pair runs cta_group::2
-//        M=256 MMAs issued by its leader: every SM holds only ITS half of B
-//        (the pair MMA reads both halves), and that half arrives as two 64-row
-//        pieces, one loaded by this CTA and one by the same-half CTA of the
-//        other pair, each multicast into both.  Per CTA and k-block: 24 KB read
-//        from L2, 32 KB written into smem, 32 KB of operands read by the
-//        tensor cores (G=3: 32 / 48 / 48) -- operand movement is what the
-//        power cap charges for (profiles/r02_gemm_geometry.txt).
-//   G=2  one CTA pair (cluster of 2) without the cross-pair multicast (A/B).
+// Every CTA owns 128 output rows x one 256-wide (or narrower) N tile:
+//   G=1  single CTA; it loads its whole B tile (launches with M <= 128).
+//   G=3  (default) cluster of 2 M-adjacent CTAs; each TMA-loads half of the
+//        weight tile and multicasts it into both (L2->SM 32 instead of 48 KB
+//        per CTA and k-block; under the power cap worth ~6% clock, r01).
+// CTA-pair geometries (cta_group::2 M=256 MMAs, alone or two pairs sharing the
+// weight tile by multicast) were built and measured in round 2: they keep the
+// tensor pipe 98% busy and read fewer operand bytes per FLOP, but their
+// launches read 2-6x the DRAM of G=3 (weight/activation panels fall out of L2)
+// and the full C3 step ran 7-11% slower at the same power cap
+// (profiles/r02_gemm_geometry.txt); they were removed.
 //
 // Epilogues: RESIDUAL adds the accumulator into the f32 residual stream with a
 // TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add, the read-modify-write
@@ -44,12 +39,6 @@
 #include "epilogue.cuh"
 #include "tc_ptx.cuh"
 
-// A/B switch for the pair geometries: 1 = plain TMA per CTA + a relayed
-// "stage landed" arrive to the pair leader instead of cta_group::2 TMA.
-#ifndef KRR_PAIR_RELAY
-#define KRR_PAIR_RELAY 0
-#endif
-
 namespace krr {
 namespace tc {
 
@@ -60,20 +49,12 @@ constexpr int STG_WARP_BYTES = 2 * STG_BUF;   // double buffered per epilogue wa
 
 template <int G> struct Geo;
 template <> struct Geo<1> {
-  static constexpr int CS = 1, MMA_CG = 1, STAGES = 4, GROUP_M = 16;
+  static constexpr int CS = 1, STAGES = 4, GROUP_M = 16;
   static constexpr int B_ROWS_SMEM = 256;     // rows of the weight tile held per CTA
 };
 template <> struct Geo<3> {
-  static constexpr int CS = 2, MMA_CG = 1, STAGES = 4, GROUP_M = 8;
+  static constexpr int CS = 2, STAGES = 4, GROUP_M = 8;
   static constexpr int B_ROWS_SMEM = 256;
-};
-template <> struct Geo<2> {
-  static constexpr int CS = 2, MMA_CG = 2, STAGES = 6, GROUP_M = 8;
-  static constexpr int B_ROWS_SMEM = 128;
-};
-template <> struct Geo<7> {
-  static constexpr int CS = 4, MMA_CG = 2, STAGES = 6, GROUP_M = 4;
-  static constexpr int B_ROWS_SMEM = 128;
 };
 constexpr int A_BYTES = 128 * BK * 2;                      // 16 KB: 128 rows per CTA
 template <int G> constexpr int b_bytes() { return Geo<G>::B_ROWS_SMEM * BK * 2; }
@@ -236,7 +217,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const __grid_constant__ CUtensorMap tmOut, int64_t M, int N, int K,
                         uint32_t idesc, int group_m, int bn, EpiParams ep) {
   using C = Geo<G>;
-  constexpr int CS = C::CS, MMA_CG = C::MMA_CG, STAGES = C::STAGES;
+  constexpr int CS = C::CS, STAGES = C::STAGES;
   constexpr int B_BYTES = b_bytes<G>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -248,42 +229,30 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* peer_full = tempty + 2;          // RELAY: peer's stage landed (leader side)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(peer_full + STAGES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CS > 1 ? cluster_rank() : 0;
-  // cta_group::2: the pair is (rank & ~1, rank | 1); its even CTA leads
-  const uint32_t pair_leader = MMA_CG == 2 ? (rank & ~1u) : rank;
-  const bool leader = rank == pair_leader;
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&peer_full[s], 1);
-      // a stage may be refilled once every MMA issuer that reads it committed:
-      // G=3 both CTAs (the peer's B slice lands here), G=7 both pair leaders
-      // (the other pair multicasts a B piece here), else this CTA's (pair's)
-      mbar_init(&empty[s], G == 3 ? 2 : G == 7 ? 2 : 1);
+      // G=3: a stage is free only when BOTH CTAs' MMAs have read it (the peer
+      // multicasts its half of B into this CTA's buffer)
+      mbar_init(&empty[s], CS);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * MMA_CG);    // every epilogue warp of the pair
+      mbar_init(&tempty[a], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    if constexpr (MMA_CG == 1) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                       smem_u32(tmem_slot)) : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                       smem_u32(tmem_slot)) : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    }
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -309,47 +278,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (elect_one_sync()) {
           uint8_t* a_dst = sA + stage * A_BYTES;
           uint8_t* b_dst = sB + stage * B_BYTES;
+          const uint32_t bar = smem_u32(&full[stage]);
+          mbar_expect_tx(&full[stage], A_BYTES + bn * BK * 2);
+          tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
           if constexpr (G == 1) {
-            const uint32_t bar = smem_u32(&full[stage]);
-            mbar_expect_tx(&full[stage], A_BYTES + bn * BK * 2);
-            tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
             tma_load<1>(b_dst, &tmB, bar, kb * BK, nb * bn);
-          } else if constexpr (G == 3) {
-            // own A rows; own slice of B multicast into both CTAs' stage buffers
+          } else {
+            // own slice of B, multicast into both CTAs' stage buffers
             const int b_rows = bn / 2;
-            const uint32_t bar = smem_u32(&full[stage]);
-            mbar_expect_tx(&full[stage], A_BYTES + bn * BK * 2);
-            tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
             tma_load_mc(b_dst + rank * (b_rows * BK * 2), &tmB, bar, kb * BK,
                         nb * bn + (int)rank * b_rows, (uint16_t)0x3);
-          } else if constexpr (KRR_PAIR_RELAY) {
-            // pair, relayed: plain TMA into this CTA's own stage and barrier; the
-            // peer's warp 1 forwards "landed" to the leader (peer_full)
-            const uint32_t bar = smem_u32(&full[stage]);
-            mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
-            tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
-            const int half = (int)(rank & 1);
-            if constexpr (G == 2) {
-              tma_load<1>(b_dst, &tmB, bar, kb * BK, nb * bn + half * 128);
-            } else {
-              const int p = (int)(rank >> 1);
-              tma_load_mc(b_dst + p * (64 * BK * 2), &tmB, bar, kb * BK,
-                          nb * bn + half * 128 + p * 64, (uint16_t)((1u << rank) | (1u << (rank ^ 2))));
-            }
-          } else {
-            // pair: every byte of both CTAs' stage lands on the pair leader's barrier
-            const uint32_t bar = mapa_rank(smem_u32(&full[stage]), pair_leader);
-            if (leader) mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
-            tma_load<2>(a_dst, &tmA, bar, kb * BK, row_a);
-            const int half = (int)(rank & 1);          // which 128-row half of the N tile
-            if constexpr (G == 2) {
-              tma_load<2>(b_dst, &tmB, bar, kb * BK, nb * bn + half * 128);
-            } else {
-              // piece p (64 rows) of this half, multicast into the same-half CTA of both pairs
-              const int p = (int)(rank >> 1);
-              tma_load_mc2(b_dst + p * (64 * BK * 2), &tmB, bar, kb * BK,
-                           nb * bn + half * 128 + p * 64, (uint16_t)((1u << rank) | (1u << (rank ^ 2))));
-            }
           }
         }
         __syncwarp();
@@ -358,63 +296,39 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     // whole warp walks the schedule; one elected lane issues (descriptors stay
-    // in uniform registers); pair geometries: the leader issues for both SMs
-    if (leader) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      const uint64_t dA = sw128_desc(smem_u32(sA));
-      const uint64_t dB = sw128_desc(smem_u32(sB));
-      // completion of a stage's MMAs frees it in every CTA that holds its operands
-      constexpr uint16_t EMPTY_MASK = G == 3 ? 0x3 : G == 7 ? 0xF : 0x0;
-      const uint16_t pair_mask = (uint16_t)(0x3u << rank);   // (leader, peer)
-      for (int tile = cid; tile < tiles; tile += ncl, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // in uniform registers, no per-MMA elect loop)
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    const uint64_t dA = sw128_desc(smem_u32(sA));
+    const uint64_t dB = sw128_desc(smem_u32(sB));
+    for (int tile = cid; tile < tiles; tile += ncl, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;   // accumulators 256 columns apart
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;   // accumulators 256 columns apart
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&full[stage], phase);
-          if constexpr (MMA_CG == 2 && KRR_PAIR_RELAY) mbar_wait(&peer_full[stage], phase);
-          tc_fence_after();
-          if (elect_one_sync()) {
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              mma_f16<MMA_CG>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
-                              dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
-            if constexpr (G == 1) mma_commit<1>(&empty[stage]);
-            else if constexpr (G == 3) mma_commit_mc1(&empty[stage], EMPTY_MASK);
-            else if constexpr (G == 2) mma_commit2_mc(&empty[stage], pair_mask);
-            else mma_commit2_mc(&empty[stage], EMPTY_MASK);
-          }
-          __syncwarp();
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
         if (elect_one_sync()) {
-          if constexpr (MMA_CG == 1) mma_commit<1>(&tfull[acc]);
-          else mma_commit2_mc(&tfull[acc], pair_mask);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_f16<1>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
+                       dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+          // completion frees the stage in every CTA that holds its operands
+          if constexpr (G == 1) mma_commit<1>(&empty[stage]);
+          else mma_commit_mc1(&empty[stage], (uint16_t)0x3);
         }
         __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-    } else if constexpr (MMA_CG == 2 && KRR_PAIR_RELAY) {
-      // the peer's idle MMA warp relays each landed stage to the leader
-      int stage = 0;
-      uint32_t phase = 0;
-      const uint32_t lead_pf = mapa_rank(smem_u32(&peer_full[0]), pair_leader);
-      for (int tile = cid; tile < tiles; tile += ncl)
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&full[stage], phase);
-          if (elect_one_sync()) mbar_arrive_cluster(lead_pf + stage * 8);
-          __syncwarp();
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
+      if (elect_one_sync()) mma_commit<1>(&tfull[acc]);
+      __syncwarp();
     }
   } else {
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     uint8_t* stg = stage_base + (warp - 2) * STG_WARP_BYTES;
-    const uint32_t tempty0 = MMA_CG == 2 ? mapa_rank(smem_u32(&tempty[0]), pair_leader)
-                                         : smem_u32(&tempty[0]);
     int it = 0, nchunk = 0;
     const bool glu = ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU;
     float gate[32];
@@ -459,7 +373,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -468,10 +382,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if constexpr (CS > 1) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    if constexpr (MMA_CG == 1)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
-    else
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
 }
 
@@ -548,8 +459,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   const int grid = std::min(CS * tiles, CS * max_clusters);
   cfg.gridDim = dim3(grid);
   cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, G>, ma, mb, mo, M, N, K, idesc, group_m, bn, ep);
-  return check_launch(G == 7 ? "gemm_tcgen05_pair_mc" : G == 2 ? "gemm_tcgen05_pair"
-                      : G == 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
+  return check_launch(G == 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
 }
 
 }  // namespace tc
@@ -567,18 +477,9 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (ep.kind == KRR_EPI_QKV_ROPE && ep.qkv.head_dim % 32 != 0)
     return launch_gemm_simt(act_dtype, A, B, M, N, K, ep, s);  // a chunk must stay in one head
 
-  // Geometry per launch (KRR_GEMM_GEO overrides for A/B: 1, 2, 3 or 7):
-  //   M <= 128          G=1 (a cluster partner would idle)
-  //   large M           G=7 (pair MMAs + cross-pair weight multicast)
-  //   otherwise         G=3
-  static const int env_geo = [] {
-    const char* e = getenv("KRR_GEMM_GEO");
-    const int v = e ? atoi(e) : 0;
-    return (v == 1 || v == 2 || v == 3 || v == 7) ? v : 0;
-  }();
-  int geo = env_geo ? env_geo : (M <= 128 ? 1 : 3);
-  if (geo == 1 && M > 128 && env_geo == 0) geo = 3;
-  // N-tile width for the cta_group::1 geometries, chosen by a wave model: each
+  // one 128-row tile: a cluster partner would idle
+  const int geo = M <= 128 ? 1 : 3;
+  // N-tile width, chosen by a wave model: each
   // candidate width bn (multiples of 32 so epilogue chunks never straddle a
   // head) gives units = m-tiles x ceil(N/bn) tiles on `slots` persistent
   // CTAs (clusters), cost = ceil(units/slots) waves x bn x c(bn), where
@@ -588,10 +489,9 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   // launches (the per-query latency batch, C2's N=2048 layers) avoid a
   // mostly-empty last wave.  Every width runs the same per-element MMA
   // sequence (full K in BK-chunk order into one fp32 accumulator), so the
-  // choice may depend on M without breaking batch invariance.  The pair
-  // geometries keep 256 (their B halves are 128 rows).
+  // choice may depend on M without breaking batch invariance.
   int bn = BN;
-  if (geo == 1 || geo == 3) {
+  {
     const int rows_per_unit = geo == 3 ? 256 : 128;
     const int64_t slots = geo == 3 ? device_sm_count() / 2 : device_sm_count();
     const int64_t m_units = (M + rows_per_unit - 1) / rows_per_unit;
@@ -602,28 +502,13 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
       if (cand == 256 || cost < best * 0.98) { best = cost; bn = cand; }
     }
   }
-  static const int env_gm = [] {
-    const char* e = getenv("KRR_GEMM_GROUP_M");
-    return e ? atoi(e) : 0;
-  }();
-  int group_m = env_gm != 0 ? env_gm          // < 0: bands of -env_gm n-tiles
-                : geo == 7 ? Geo<7>::GROUP_M : geo == 2 ? Geo<2>::GROUP_M
-                : geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
-  if (env_gm == 0 && (geo == 2 || geo == 7)) {
-    // pair geometries: keep the weights L2-resident and stream activations --
-    // the whole weight matrix when it fits (QKV, WO: all n-tiles in one band),
-    // else bands of 16 n-tiles when those fit (MLP-up), else M-groups (MLP-down)
-    const double wbytes = (double)N * K * 2;
-    const int num_n = (N + bn - 1) / bn;
-    if (wbytes <= 64.0 * (1 << 20)) group_m = -num_n;
-    else if (16.0 * bn * K * 2 <= 40.0 * (1 << 20)) group_m = -16;
-  }
+  const int group_m = geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
   const CUtensorMapDataType dt =
       act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap ma, mb, mo;
   int rc = make_map(&ma, A, dt, 2, (uint64_t)K, (uint64_t)M, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  const uint32_t b_box = geo == 1 ? bn : geo == 3 ? bn / 2 : geo == 2 ? 128 : 64;
+  const uint32_t b_box = geo == 1 ? bn : bn / 2;
   rc = make_map(&mb, B, dt, 2, (uint64_t)K, (uint64_t)N, BK, b_box, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   if (ep.kind == KRR_EPI_RESIDUAL) {
@@ -643,19 +528,13 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (rc) return rc;
   // instruction descriptor: D=f32 @4, A/B f16|bf16 @7/@10, K-major both, N>>3 @17, M>>4 @24
   const uint32_t fmt = act_dtype == KRR_BF16 ? 1u : 0u;
-  const int mma_m = (geo == 2 || geo == 7) ? 256 : 128;
   const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(bn >> 3) << 17) |
-                         ((uint32_t)(mma_m >> 4) << 24);
-#define KRR_GEO_LAUNCH(T)                                                             \
-  switch (geo) {                                                                      \
-    case 1: return launch<T, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);      \
-    case 2: return launch<T, 2>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);      \
-    case 7: return launch<T, 7>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);      \
-    default: return launch<T, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);     \
-  }
-  if (act_dtype == KRR_F16) { KRR_GEO_LAUNCH(__half) }
-  KRR_GEO_LAUNCH(__nv_bfloat16)
-#undef KRR_GEO_LAUNCH
+                         ((uint32_t)(128 >> 4) << 24);
+  if (act_dtype == KRR_F16)
+    return geo == 1 ? launch<__half, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
+                    : launch<__half, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);
+  return geo == 1 ? launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
+                  : launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);
 }
 
 }  // namespace krr

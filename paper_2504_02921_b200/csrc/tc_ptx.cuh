@@ -63,48 +63,6 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// L2 eviction-priority policies for TMA loads (createpolicy): operands read
-// by many CTAs over a long window (weights) vs streamed once per tile row.
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-template <int CG>
-__device__ __forceinline__ void tma_load_hint(void* dst, const CUtensorMap* map, uint32_t bar,
-                                              int c0, int c1, uint64_t policy) {
-  if constexpr (CG == 1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
-  } else {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tma_load_mc_hint(void* dst, const CUtensorMap* map, uint32_t bar,
-                                                 int c0, int c1, uint16_t mask, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
-      : "memory");
-}
 template <int CG>
 __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint32_t bar,
                                          int c0, int c1) {
@@ -278,25 +236,6 @@ __device__ __forceinline__ void tma_load_mc(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void mma_commit_mc1(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-// cta_group::2 TMA load multicast to the CTAs in ctaMask; the completion of
-// each destination lands on the mbarrier at `bar`'s offset in the LEADER CTA
-// of that destination's pair (bar = this CTA's barrier address with the peer
-// bit cleared, i.e. a shared::cluster address in the pair leader).
-__device__ __forceinline__ void tma_load_mc2(void* dst, const CUtensorMap* map, uint32_t bar,
-                                             int c0, int c1, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-// cta_group::2 MMA completion arriving on the same mbarrier of every CTA in mask.
-__device__ __forceinline__ void mma_commit2_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }

@@ -285,11 +285,20 @@ def run_host_tier(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     preset, corpus, nq, nc, keep = CONFIGS[args.config]
-    corpus = args.corpus or corpus
-    nq = args.queries or nq
-    nc = min(args.cands or nc, corpus)
     cfg, lay = PRESETS[preset]
     D = lay.document_len
+    if args.corpus < 0:
+        # tier sized from the host's free RAM (a corpus larger than
+        # HBM, capped by box RAM): 60% of available, at most 400 GB
+        import psutil
+        elems = 2 * cfg.layers * cfg.kv_heads * D * cfg.head_dim
+        page = {None: 2 * elems, "int8": elems, "int4": elems // 2}[args.host_quant or None] \
+            + (4 * 2 * cfg.layers * cfg.kv_heads * cfg.head_dim if args.host_quant else 0)
+        corpus = int(min(0.6 * psutil.virtual_memory().available, 400e9) // page)
+    else:
+        corpus = args.corpus or corpus
+    nq = args.queries or nq
+    nc = min(args.cands or nc, corpus)
     model = krr.RerankModel.build(cfg, lay, precision=args.precision, device=dev)
     w = model.weights
     # ---- corpus: prefill in HBM chunks, park every page in the pinned tier
@@ -382,6 +391,8 @@ def run_host_tier(args, rank, world, local_rank):
                                   f"{corpus}-doc pinned host tier ({page * corpus / 1e9:.1f} GB, "
                                   f"{args.host_quant or 'f16'}), streamed H2D per step",
                       "host_docs": corpus, "page_bytes_over_pcie": page,
+                      "host_tier_gb": page * corpus / 1e9,
+                      "hbm_gb": torch.cuda.get_device_properties(dev).total_memory / 1e9,
                       "host_quant": args.host_quant or None},
            "h2d_peak_gbs": h2d_peak, "query_len_sweep": sweep}
     if rank == 0:
@@ -680,7 +691,9 @@ def main():
     # f16 operands (fp32 accumulation): the precision that meets north_star's 2e-2
     # gate; bf16 misses it on this model (tests/test_gpu_parity_wide.py)
     ap.add_argument("--precision", default="f16", choices=["f16"])
-    ap.add_argument("--corpus", type=int, default=0)
+    ap.add_argument("--corpus", type=int, default=0,
+                    help="corpus docs (0 = the config's default; C5: -1 sizes the pinned "
+                         "host tier from free RAM)")
     ap.add_argument("--queries", type=int, default=0)
     ap.add_argument("--cands", type=int, default=0)
     ap.add_argument("--latency-reps", type=int, default=20)

@@ -194,6 +194,29 @@ class KVPool:
         return np.ascontiguousarray(page[:, 0]), np.ascontiguousarray(page[:, 1])
 
 
+class PinnedRows:
+    """``n`` rows of ``row_shape`` in pinned host memory, allocated in chunks of
+    at most ``chunk_bytes`` (a tier larger than HBM -- hundreds of GB -- is not
+    one cudaHostAlloc).  ``rows[h]`` is row h as a tensor view."""
+
+    def __init__(self, n: int, row_shape, dtype, chunk_bytes: int = 4 << 30):
+        import torch
+        self.n, self.row_shape, self.dtype = n, tuple(row_shape), dtype
+        row_bytes = int(np.prod(row_shape)) * torch.empty((), dtype=dtype).element_size()
+        self.per_chunk = max(1, min(n, chunk_bytes // max(row_bytes, 1)))
+        self.chunks = []
+        for c0 in range(0, n, self.per_chunk):
+            rows = min(self.per_chunk, n - c0)
+            self.chunks.append(torch.empty((rows, *self.row_shape), dtype=dtype,
+                                           pin_memory=True))
+        self.nbytes = n * row_bytes
+
+    def __getitem__(self, h: int):
+        if not 0 <= h < self.n:
+            raise IndexError(h)
+        return self.chunks[h // self.per_chunk][h % self.per_chunk]
+
+
 class HostKVTier:
     """Pinned host-DRAM tier with the pool's slot layout, streamed into an HBM
     staging pool on a side stream (cudaMemcpyAsync via torch copy_).
@@ -218,18 +241,15 @@ class HostKVTier:
         L, _, KVH, D, HD = self.page_shape
         self.n_tensors, self.tensor_elems = 2 * L, KVH * D * HD
         if quant is None:
-            self.slab = torch.empty((capacity, *self.page_shape), dtype=self.dtype,
-                                    pin_memory=True)
+            self.slab = PinnedRows(capacity, self.page_shape, self.dtype)
             self.slot_bytes = pool_like.slot_bytes
         else:
             bits = self.BITS[quant]
             tb = self.tensor_elems if bits == 8 else (self.tensor_elems + 1) // 2
             self.code_bytes = self.n_tensors * tb
             self.scale_elems = self.n_tensors * KVH * HD
-            self.codes = torch.empty((capacity, self.code_bytes), dtype=torch.uint8,
-                                     pin_memory=True)
-            self.scales = torch.empty((capacity, self.scale_elems), dtype=torch.float32,
-                                      pin_memory=True)
+            self.codes = PinnedRows(capacity, (self.code_bytes,), torch.uint8)
+            self.scales = PinnedRows(capacity, (self.scale_elems,), torch.float32)
             self.slot_bytes = self.code_bytes + 4 * self.scale_elems   # bytes over PCIe
         self.valid_len = np.zeros(capacity, dtype=np.int64)
         self._by_id: dict[str, int] = {}

@@ -20,6 +20,8 @@
  *   krr_gemm              <- model.py:368,397,400 x@wqkv (+RoPE :370-371), attn@wo (+residual),
  *                            gelu(xn@w_up) (:444-446), @w_down (+residual)
  *   krr_attention         <- model.py:373-394 (+ _exp_rows :406-436)
+ *   krr_attention_quant   <- the same over HRKV INT8/INT4 prefix pages, codec.py:82-95
+ *                            dequantize_tensor fused in (pipeline.py:251-271 fetch+decode)
  *   krr_score_head        <- model.py:402 final norm + reranker.py:211-212 last-row dot
  *   krr_segmented_topk    <- pipeline.py:285-287 _select
  *   krr_dequant_kv        <- codec.py:82-95 dequantize_tensor (INT8/INT4 -> 16-bit pool page)
@@ -143,6 +145,13 @@ typedef struct {
   /* device [n_seqs*seq_len] absolute positions (RoPE), or NULL = pos0 + t;
    * the caller checks them against max_position */
   const int32_t* positions;
+  /* prefix page format: 0/16 = act-dtype pages; 8 / 4 = HRKV INT8 / INT4 code
+   * pages (codec.py:58-115; slot layout [L][2][KVH][prefix_len][head_dim] codes,
+   * INT4 low nibble first) with f32 scales [page][head_dim] at prefix_scales,
+   * page = (slot*L + layer)*2*KVH + {K,V}*KVH + kvh, dequantised inside the
+   * attention kernel (head_dim 64|128, 16-bit activations) */
+  int32_t prefix_bits;
+  const float* prefix_scales;
 } krr_batch_t;
 
 const char* krr_last_error(void);
@@ -190,6 +199,17 @@ int krr_attention(int backend, int act_dtype, const void* q, int32_t n_seqs, int
                   const uint8_t* tok_valid, void* out, const void* prefix_pool,
                   int64_t prefix_pool_bytes, const void* cur_pool, int64_t cur_pool_bytes,
                   krr_stream_t stream);
+/* krr_attention over quantised prefix pages (prefix_bits 8|4, see krr_batch_t):
+ * codec.py:82-95 dequantize_tensor fused into model.py:373-394 -- the codes are
+ * expanded to f16(code*scale) in shared memory, never written back to HBM. */
+int krr_attention_quant(int backend, int act_dtype, const void* q, int32_t n_seqs,
+                        int32_t kv_heads, int32_t group, int32_t head_dim, int32_t seq_len,
+                        int32_t prefix_len, int32_t layer, int32_t cur_layer,
+                        void* const* prefix_kv, const int32_t* prefix_valid_len,
+                        void* const* cur_kv, const uint8_t* tok_valid, void* out,
+                        const void* prefix_pool, int64_t prefix_pool_bytes, const void* cur_pool,
+                        int64_t cur_pool_bytes, int32_t prefix_bits, const float* prefix_scales,
+                        krr_stream_t stream);
 /* Co-resident CTAs per SM of the tcgen05 attention kernel (diagnostic). */
 int krr_attention_occupancy(int act_dtype, int32_t head_dim, int32_t* ctas_per_sm);
 /* model.py:402 final norm + reranker.py:211-212 score of the last valid row

@@ -27,7 +27,7 @@ ATTN_TC = ATTN_MMA
 EXPORTS = (
     "krr_last_error", "krr_version", "krr_launch_count", "krr_workspace_bytes", "krr_forward",
     "krr_profile_enable", "krr_profile_read", "krr_init_uniform", "krr_embed", "krr_rmsnorm",
-    "krr_gemm", "krr_attention", "krr_attention_occupancy", "krr_score_head", "krr_segmented_topk", "krr_dequant_kv",
+    "krr_gemm", "krr_attention", "krr_attention_quant", "krr_attention_occupancy", "krr_score_head", "krr_segmented_topk", "krr_dequant_kv",
     "krr_quant_pages", "krr_dequant_pages",
 )
 
@@ -56,7 +56,8 @@ class Batch(C.Structure):
                 ("cur_kv_layers", i32), ("tokens", vp), ("tok_valid", vp), ("prefix_valid_len", vp),
                 ("prefix_kv", vp), ("cur_kv", vp), ("last_index", vp), ("scores", vp),
                 ("prefix_pool", vp), ("prefix_pool_bytes", i64), ("cur_pool", vp),
-                ("cur_pool_bytes", i64), ("x_in", vp), ("x_out", vp), ("positions", vp)]
+                ("cur_pool_bytes", i64), ("x_in", vp), ("x_out", vp), ("positions", vp),
+                ("prefix_bits", i32), ("prefix_scales", vp)]
 
 
 _LIB = None
@@ -85,6 +86,9 @@ def lib():
                                C.POINTER(QKV), vp]
         L.krr_attention.argtypes = [C.c_int, C.c_int, vp, i32, i32, i32, i32, i32, i32, i32,
                                     i32, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp]
+        L.krr_attention_quant.argtypes = [C.c_int, C.c_int, vp, i32, i32, i32, i32, i32, i32,
+                                          i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, i64, i32,
+                                          vp, vp]
         L.krr_attention_occupancy.argtypes = [C.c_int, i32, C.POINTER(i32)]
         L.krr_score_head.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp]
         L.krr_segmented_topk.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]

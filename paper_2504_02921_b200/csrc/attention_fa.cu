@@ -16,8 +16,17 @@
 //  * the suffix-block mask (tok_valid, causal) comes from a 64-bit ballot mask,
 //    not per-key global loads.
 //
-// Work item = (unit, pair of 128-row tiles) as in attention_pp.cu.
+// Work item = (unit, pair of 128-row tiles).
 // SMEM: Q_A|Q_B 64 KB, K ring 4 x 16 KB, V ring 4 x 16 KB = 192 KB.
+//
+// Quantised prefix pages (QB = 8 | 4: HRKV INT8/INT4 codes, codec.py:58-115,
+// per-(kv_head, channel) f32 scales) are dequantised inside the kernel: the
+// producer lands each 64-key block of codes by TMA into a small code ring
+// (2 x 8 KB per K/V at INT8), and two converter warps (w10 K, w11 V) expand
+// it into the same 128B-swizzled 16-bit K/V ring slots the MMAs read,
+// f16(code * scale) exactly as krr_dequant_pages rounds it -- so the fused
+// path is bit-identical to "dequantise the page into HBM, then attend" while
+// only the codes cross HBM (2x / 4x fewer bytes) and no expand pass runs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math_constants.h>
@@ -44,6 +53,8 @@ constexpr int TM = 128;
 constexpr int KB = 64;
 constexpr int NK = 4, NV = 4;   // K / V ring depth
 constexpr int THREADS = 320;    // w0 producers (lanes 0 Q, 1 K, 2 V), w1 MMA, w2-5 / w6-9 softmax
+constexpr int NC = 2;           // code ring depth per K / V (quantised prefix)
+template <int QB> constexpr int threads_of() { return QB == 16 ? THREADS : THREADS + 64; }
 constexpr float RESCALE_LOG2 = 15.0f;   // P <= 2^15 < f16 max
 
 struct Params {
@@ -56,10 +67,11 @@ struct Params {
   const int32_t* prefix_valid_len;
   const uint8_t* tok_valid;
   void* out;
+  const float* scales;   // quantised prefix: [page][HD] f32 (page as in the code pool)
   int KVH, G, T, P, layer, cur_layer, R, pairs, items;
 };
 
-template <int HD>
+template <int HD, int QB = 16>
 struct Smem {
   static constexpr int ATOM_Q = TM * 128;                // one 128-row swizzle column of Q
   static constexpr int ATOM_KV = KB * 128;               // one 128-key swizzle column of K/V
@@ -68,7 +80,10 @@ struct Smem {
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + 2 * Q_TILE;
   static constexpr int V_OFF = K_OFF + NK * KV_BYTES;
-  static constexpr int BAR_OFF = V_OFF + NV * KV_BYTES;
+  static constexpr int CODE_ROW = HD * QB / 8;           // code bytes per key (QB < 16)
+  static constexpr int CODE_BLK = KB * CODE_ROW;
+  static constexpr int C_OFF = V_OFF + NV * KV_BYTES;    // code rings [K|V][NC]
+  static constexpr int BAR_OFF = C_OFF + (QB < 16 ? 2 * NC * CODE_BLK : 0);
   static constexpr int TOTAL = BAR_OFF + 512;
   static_assert(2 * KB + HD <= 256, "TMEM budget per tile");
 };
@@ -77,7 +92,7 @@ enum {
   B_QFULL = 0, B_QEMPTY, B_KFULL, B_KEMPTY = B_KFULL + NK, B_VFULL = B_KEMPTY + NK,
   B_VEMPTY = B_VFULL + NV, B_SFULL = B_VEMPTY + NV /*[tile][buf]*/, B_PFULL = B_SFULL + 4,
   B_PVDONE = B_PFULL + 4 /*[tile][buf]*/, B_ODONE = B_PVDONE + 4, B_OEMPTY = B_ODONE + 2,
-  B_COUNT = B_OEMPTY + 2
+  B_CFULL = B_OEMPTY + 2 /*[K|V][NC]*/, B_CEMPTY = B_CFULL + 2 * NC, B_COUNT = B_CEMPTY + 2 * NC
 };
 
 template <typename T>
@@ -119,12 +134,40 @@ __device__ __forceinline__ Item item_of(const Params& p, int it) {
   return x;
 }
 
-template <typename T, int HD>
-__global__ void __launch_bounds__(THREADS, 1)
+// Decode one 16-byte chunk of HRKV codes (16 INT8 or 32 INT4, low nibble
+// first) into 16-bit values f16(code * scale) -- the rounding of
+// krr_dequant_pages.  code + bias is built exactly as the f32 2^23 + u and
+// the bias subtracted (one PRMT/LOP + FADD per element, no I2F).
+template <typename T, int QB>
+__device__ __forceinline__ void decode_chunk(const uint4 v, const float* sc, uint32_t* out) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if constexpr (QB == 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t wx = w[i >> 1] ^ 0x80808080u;            // byte -> code + 128
+      const int b0 = (i & 1) * 2;
+      const float f0 = __uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7440u + b0)) - 8388736.f;
+      const float f1 = __uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7441u + b0)) - 8388736.f;
+      out[i] = pack_2<T>(f0 * sc[2 * i], f1 * sc[2 * i + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t wx = w[i >> 2] ^ 0x88888888u;            // nibble -> code + 8
+      const int sh = (i & 3) * 8;
+      const float f0 = __uint_as_float(0x4B000000u | ((wx >> sh) & 0xFu)) - 8388616.f;
+      const float f1 = __uint_as_float(0x4B000000u | ((wx >> (sh + 4)) & 0xFu)) - 8388616.f;
+      out[i] = pack_2<T>(f0 * sc[2 * i], f1 * sc[2 * i + 1]);
+    }
+  }
+}
+
+template <typename T, int HD, int QB>
+__global__ void __launch_bounds__(threads_of<QB>(), 1)
     attn_fa_kernel(const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmPre,
                    const __grid_constant__ CUtensorMap tmCur, const Params p) {
-  using S = Smem<HD>;
+  using S = Smem<HD, QB>;
   extern __shared__ uint8_t smem[];
   uint8_t* sQ = smem + S::Q_OFF;
   uint8_t* sK = smem + S::K_OFF;
@@ -150,6 +193,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int x = 0; x < 2; ++x) {
       mbar_init(&bar[B_ODONE + x], 1);
       mbar_init(&bar[B_OEMPTY + x], 4);
+    }
+    for (int c = 0; c < 2 * NC; ++c) {
+      mbar_init(&bar[B_CFULL + c], 1);
+      mbar_init(&bar[B_CEMPTY + c], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -185,7 +232,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint64_t* full = &bar[is_k ? B_KFULL : B_VFULL];
       uint64_t* empty = &bar[is_k ? B_KEMPTY : B_VEMPTY];
       uint8_t* ring = is_k ? sK : sV;
-      int g = 0;
+      const int cw = is_k ? 0 : 1;
+      uint8_t* cring = smem + S::C_OFF + cw * NC * S::CODE_BLK;
+      int g = 0, gc = 0;
       for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
         const Item x = item_of(p, it);
         const int pre_page = p.P ? (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b]) -
@@ -196,10 +245,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                                    p.cur_page_bytes) + (p.cur_layer * 2) * p.KVH + x.kvh;
         const int vofs = is_k ? 0 : p.KVH;
         for (int j = 0; j < x.nb; ++j, ++g) {
+          const bool pre = j < x.nb_pre;
+          if (QB < 16 && pre) {          // codes -> code ring; a converter warp fills K/V
+            const int c = gc % NC;
+            mbar_wait(&bar[B_CEMPTY + cw * NC + c], ((gc / NC) & 1) ^ 1);
+            mbar_expect_tx(&bar[B_CFULL + cw * NC + c], S::CODE_BLK);
+            tma_load3(cring + c * S::CODE_BLK, &tmPre, &bar[B_CFULL + cw * NC + c], 0, j * KB,
+                      pre_page + vofs);
+            ++gc;
+            continue;
+          }
           const int s = g % nst;
           mbar_wait(&empty[s], ((g / nst) & 1) ^ 1);
           mbar_expect_tx(&full[s], S::KV_BYTES);
-          const bool pre = j < x.nb_pre;
           const CUtensorMap* map = pre ? &tmPre : &tmCur;
           const int key0 = (pre ? j : j - x.nb_pre) * KB;
           const int pk = (pre ? pre_page : cur_page) + vofs;
@@ -293,6 +351,65 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
       }
       g += x.nb;
+    }
+  } else if (warp >= 10) {
+    // ---------------------------------------------------------- converters (QB < 16)
+    if constexpr (QB < 16) {
+      const int cw = warp - 10;                        // 0: K, 1: V
+      uint64_t* full = &bar[cw == 0 ? B_KFULL : B_VFULL];
+      uint64_t* empty = &bar[cw == 0 ? B_KEMPTY : B_VEMPTY];
+      uint8_t* ring = cw == 0 ? sK : sV;
+      const uint8_t* cring = smem + S::C_OFF + cw * NC * S::CODE_BLK;
+      constexpr int CPR = S::CODE_ROW / 16;            // 16-byte code chunks per key
+      constexpr int CH = 128 / QB;                     // channels per code chunk
+      constexpr int RSTEP = 32 / CPR;
+      static_assert(CPR >= 1 && CPR <= 32 && KB % RSTEP == 0, "code chunk mapping");
+      const int cc = lane % CPR, r0 = lane / CPR;
+      float sc[CH];
+      int g = 0, gc = 0;
+      for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+        const Item x = item_of(p, it);
+        if (x.nb_pre > 0) {
+          const int page = (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b]) -
+                                  p.prefix_base) / p.prefix_page_bytes) +
+                           (p.layer * 2 + cw) * p.KVH + x.kvh;
+          const float4* s4 = reinterpret_cast<const float4*>(p.scales + (int64_t)page * HD +
+                                                             cc * CH);
+#pragma unroll
+          for (int i = 0; i < CH / 4; ++i) {
+            const float4 f = __ldg(s4 + i);
+            sc[4 * i] = f.x; sc[4 * i + 1] = f.y; sc[4 * i + 2] = f.z; sc[4 * i + 3] = f.w;
+          }
+        }
+        for (int j = 0; j < x.nb_pre; ++j, ++gc) {
+          const int gg = g + j, s = gg % NK, c = gc % NC;
+          mbar_wait(&bar[B_CFULL + cw * NC + c], (gc / NC) & 1);
+          mbar_wait(&empty[s], ((gg / NK) & 1) ^ 1);
+          const uint8_t* src = cring + c * S::CODE_BLK;
+          uint8_t* dst = ring + s * S::KV_BYTES;
+#pragma unroll 2
+          for (int r = r0; r < KB; r += RSTEP) {
+            const uint4 v = *reinterpret_cast<const uint4*>(src + r * S::CODE_ROW + cc * 16);
+            uint32_t o[CH / 2];
+            decode_chunk<T, QB>(v, sc, o);
+#pragma unroll
+            for (int oc = 0; oc < CH / 8; ++oc) {      // 8 channels = one 16-byte chunk
+              const int ch = cc * CH + oc * 8;
+              const int k = (ch & 63) >> 3;
+              *reinterpret_cast<uint4*>(dst + (ch >> 6) * S::ATOM_KV + r * 128 +
+                                        ((k ^ (r & 7)) << 4)) =
+                  make_uint4(o[4 * oc], o[4 * oc + 1], o[4 * oc + 2], o[4 * oc + 3]);
+            }
+          }
+          fence_async_smem();                          // generic writes -> tensor-core reads
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&full[s]);
+            mbar_arrive(&bar[B_CEMPTY + cw * NC + c]);
+          }
+        }
+        g += x.nb;
+      }
     }
   } else {
     // ---------------------------------------------------------- softmax WGs
@@ -464,21 +581,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 }
 
 static int encode(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int rank,
-                  const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
+                  const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                  CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = encoder();
   if (!enc) return fail(KRR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(map, dt, rank, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(KRR_ECUDA, "attention tensor map encode failed: " + std::to_string((int)r));
   return KRR_OK;
 }
 
-template <typename T, int HD>
+template <typename T, int HD, int QB>
 static int launch(const AttnParams& a, cudaStream_t s) {
-  using Sm = Smem<HD>;
+  using Sm = Smem<HD, QB>;
   const CUtensorMapDataType dt = std::is_same<T, __half>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                                 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const int R = a.group * a.seq_len;
@@ -503,8 +621,21 @@ static int launch(const AttnParams& a, cudaStream_t s) {
     int rc = encode(&mc, a.cur_pool, dt, 3, dims, str, box);
     if (rc) return rc;
   }
-  const int64_t pre_page = (int64_t)std::max(a.prefix_len, 1) * HD * sizeof(T);
-  if (a.prefix_len > 0) {
+  // 16-bit pages, or HRKV code pages ([key][HD*QB/8] bytes, no swizzle: the
+  // converter warps read them with plain loads)
+  const int64_t pre_row = QB == 16 ? (int64_t)HD * sizeof(T) : (int64_t)HD * QB / 8;
+  const int64_t pre_page = (int64_t)std::max(a.prefix_len, 1) * pre_row;
+  if (QB < 16) {
+    KRR_REQUIRE(a.prefix_len > 0 && a.prefix_scales != nullptr, KRR_ECONFIG,
+                "quantised prefix pages need prefix_len > 0 and scales");
+    cuuint64_t dims[3] = {(cuuint64_t)pre_row, (cuuint64_t)a.prefix_len,
+                          (cuuint64_t)(a.prefix_pool_bytes / pre_page)};
+    cuuint64_t str[2] = {(cuuint64_t)pre_row, (cuuint64_t)pre_page};
+    cuuint32_t box[3] = {(cuuint32_t)pre_row, (cuuint32_t)KB, 1};
+    int rc = encode(&mp, a.prefix_pool, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, dims, str, box,
+                    CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+  } else if (a.prefix_len > 0) {
     cuuint64_t dims[3] = {(cuuint64_t)HD, (cuuint64_t)a.prefix_len,
                           (cuuint64_t)(a.prefix_pool_bytes / pre_page)};
     cuuint64_t str[2] = {(cuuint64_t)HD * sizeof(T), (cuuint64_t)pre_page};
@@ -517,14 +648,14 @@ static int launch(const AttnParams& a, cudaStream_t s) {
   const int items = (int)(units * pairs);
   Params p{a.prefix_kv, static_cast<const char*>(a.prefix_pool), pre_page, a.cur_kv,
            static_cast<const char*>(a.cur_pool), cur_page, a.prefix_valid_len, a.tok_valid,
-           a.out, a.kv_heads, a.group, a.seq_len, a.prefix_len, a.layer, a.cur_layer, R,
-           pairs, items};
+           a.out, a.prefix_scales, a.kv_heads, a.group, a.seq_len, a.prefix_len, a.layer,
+           a.cur_layer, R, pairs, items};
   {
-    const int rc = ensure_func_smem((const void*)attn_fa_kernel<T, HD>, Sm::TOTAL);
+    const int rc = ensure_func_smem((const void*)attn_fa_kernel<T, HD, QB>, Sm::TOTAL);
     if (rc) return rc;
   }
   const int grid = std::min(items, device_sm_count());
-  attn_fa_kernel<T, HD><<<grid, THREADS, Sm::TOTAL, s>>>(mq, mp, mc, p);
+  attn_fa_kernel<T, HD, QB><<<grid, threads_of<QB>(), Sm::TOTAL, s>>>(mq, mp, mc, p);
   return check_launch("attention_fa");
 }
 
@@ -536,13 +667,25 @@ extern "C" int krr_fa_trace_read(unsigned long long* out) {
 }
 #endif
 
+template <typename T, int QB>
+static int launch_hd(const AttnParams& p, cudaStream_t s) {
+  return p.head_dim == 64 ? attn_fa::launch<T, 64, QB>(p, s) : attn_fa::launch<T, 128, QB>(p, s);
+}
+
 int launch_attention_fa(int act_dtype, const AttnParams& p, cudaStream_t s) {
   if (!attention_tcgen05_supported(act_dtype, p) || p.head_dim > 128)
     return fail(KRR_EUNSUPPORTED, "TMEM-P attention needs f16/bf16, head_dim 64|128 and pool bases");
-  if (act_dtype == KRR_F16)
-    return p.head_dim == 64 ? attn_fa::launch<__half, 64>(p, s) : attn_fa::launch<__half, 128>(p, s);
-  return p.head_dim == 64 ? attn_fa::launch<__nv_bfloat16, 64>(p, s)
-                          : attn_fa::launch<__nv_bfloat16, 128>(p, s);
+  const int qb = p.prefix_bits == 0 ? 16 : p.prefix_bits;
+  if (qb != 16 && qb != 8 && qb != 4)
+    return fail(KRR_ECONFIG, "prefix_bits must be 16 (or 0), 8 or 4");
+  if (act_dtype == KRR_F16) {
+    if (qb == 8) return launch_hd<__half, 8>(p, s);
+    if (qb == 4) return launch_hd<__half, 4>(p, s);
+    return launch_hd<__half, 16>(p, s);
+  }
+  if (qb == 8) return launch_hd<__nv_bfloat16, 8>(p, s);
+  if (qb == 4) return launch_hd<__nv_bfloat16, 4>(p, s);
+  return launch_hd<__nv_bfloat16, 16>(p, s);
 }
 
 }  // namespace krr

@@ -504,6 +504,13 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
     else backend = mma_hd ? KRR_ATTN_MMA : KRR_ATTN_SIMT;   // any other head_dim
   }
   ProfScope ps(s, 1);
+  if (p.prefix_bits != 0 && p.prefix_bits != 16) {
+    // quantised prefix pages are expanded inside the TMEM-P kernel only
+    if (backend != KRR_ATTN_TCGEN05 || p.head_dim > 128)
+      return fail(KRR_EUNSUPPORTED, "quantised prefix pages need the tcgen05 attention with "
+                                    "head_dim 64|128 and 16-bit activations");
+    return launch_attention_fa(act, p, s);
+  }
   if (backend == KRR_ATTN_TCGEN05) {
     // head_dim 256 (Gemma shape) uses the one-tile kernel: its O accumulator
     // needs 256 TMEM columns, leaving no room for a second tile's S/P
@@ -632,9 +639,23 @@ int krr_attention(int backend, int act_dtype, const void* q, int32_t n_seqs, int
                   const uint8_t* tok_valid, void* out, const void* prefix_pool,
                   int64_t prefix_pool_bytes, const void* cur_pool, int64_t cur_pool_bytes,
                   krr_stream_t stream) {
+  return krr_attention_quant(backend, act_dtype, q, n_seqs, kv_heads, group, head_dim, seq_len,
+                             prefix_len, layer, cur_layer, prefix_kv, prefix_valid_len, cur_kv,
+                             tok_valid, out, prefix_pool, prefix_pool_bytes, cur_pool,
+                             cur_pool_bytes, 16, nullptr, stream);
+}
+
+int krr_attention_quant(int backend, int act_dtype, const void* q, int32_t n_seqs,
+                        int32_t kv_heads, int32_t group, int32_t head_dim, int32_t seq_len,
+                        int32_t prefix_len, int32_t layer, int32_t cur_layer,
+                        void* const* prefix_kv, const int32_t* prefix_valid_len,
+                        void* const* cur_kv, const uint8_t* tok_valid, void* out,
+                        const void* prefix_pool, int64_t prefix_pool_bytes, const void* cur_pool,
+                        int64_t cur_pool_bytes, int32_t prefix_bits, const float* prefix_scales,
+                        krr_stream_t stream) {
   AttnParams p{q, n_seqs, kv_heads, group, head_dim, seq_len, prefix_len, layer, cur_layer,
                prefix_kv, prefix_valid_len, cur_kv, tok_valid, out, prefix_pool,
-               prefix_pool_bytes, cur_pool, cur_pool_bytes};
+               prefix_pool_bytes, cur_pool, cur_pool_bytes, prefix_bits, prefix_scales};
   if (n_seqs == 0) return KRR_OK;
   return do_attention(backend, act_dtype, p, (cudaStream_t)stream);
 }
@@ -829,7 +850,8 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     if (prefill_only && l == L - 1) break;
     AttnParams ap{qb, b->n_seqs, KVH, G, HD, b->seq_len, b->prefix_len, l, cl,
                   b->prefix_kv, b->prefix_valid_len, b->cur_kv, b->tok_valid, ab,
-                  b->prefix_pool, b->prefix_pool_bytes, b->cur_pool, b->cur_pool_bytes};
+                  b->prefix_pool, b->prefix_pool_bytes, b->cur_pool, b->cur_pool_bytes,
+                  b->prefix_bits, b->prefix_scales};
     rc = do_attention(m->attn_backend, act, ap, s);
     if (rc) return rc;
     EpiParams er{};

@@ -32,6 +32,11 @@ struct AttnParams {
   int64_t prefix_pool_bytes;
   const void* cur_pool;
   int64_t cur_pool_bytes;
+  // prefix page element: 16-bit (0 or 16), or HRKV INT8 / INT4 codes (8 / 4)
+  // with per-(page, channel) f32 scales [page][head_dim]; pages then hold
+  // prefix_len * head_dim * bits / 8 bytes and prefix_pool is the code pool
+  int prefix_bits;
+  const float* prefix_scales;
 };
 int launch_attention_mma(int act_dtype, const AttnParams& p, cudaStream_t s);
 int launch_attention_tcgen05(int act_dtype, const AttnParams& p, cudaStream_t s);

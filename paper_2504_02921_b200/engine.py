@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError
-from .kvpool import KVPool
+from .kvpool import CodePages, KVPool
 from .model import DeviceWeights
 
 DEFAULT_WORKSPACE_BUDGET = 32 << 30  # bytes of activations per krr_forward call
@@ -88,12 +88,15 @@ def _extent(t):
 def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
                 prefix_valid, prefix_ptrs, cur_ptrs, cur_kv_layers: int, last_index=None,
                 scores=None, stream=None, prefix_pool=None, cur_pool=None, x_in=None,
-                x_out=None, ws: "_Workspace | None" = None, positions=None) -> None:
+                x_out=None, ws: "_Workspace | None" = None, positions=None,
+                prefix_bits: int = 0, prefix_scales=None) -> None:
     """One krr_forward call over n sequences (all device tensors, contiguous):
     tokens int32 [n, T], tok_valid uint8 [n, T], prefix_valid int32 [n],
     prefix_ptrs / cur_ptrs int64 [n], last_index int32 [n], scores f32 [n].
     ``prefix_pool`` / ``cur_pool`` are the tensors those pointers point into
-    (pool slab, suffix scratch); they let attention address pages via TMA."""
+    (pool slab, suffix scratch); they let attention address pages via TMA.
+    ``prefix_bits`` 8 / 4: the prefix pages are HRKV INT8 / INT4 codes with f32
+    ``prefix_scales`` (kvpool.CodePages), dequantised inside attention."""
     import torch
     n, T = tokens.shape
     if n == 0:
@@ -105,7 +108,8 @@ def run_forward(w: DeviceWeights, tokens, tok_valid, pos0: int, prefix_len: int,
     cp, cb = _extent(cur_pool)
     b = _lib.Batch(n, T, pos0, prefix_len, cur_kv_layers, _ptr(tokens), _ptr(tok_valid),
                    _ptr(prefix_valid), _ptr(prefix_ptrs), _ptr(cur_ptrs), _ptr(last_index),
-                   _ptr(scores), pp, pb, cp, cb, _ptr(x_in), _ptr(x_out), _ptr(positions))
+                   _ptr(scores), pp, pb, cp, cb, _ptr(x_in), _ptr(x_out), _ptr(positions),
+                   prefix_bits, _ptr(prefix_scales))
     if stream is None:
         stream = torch.cuda.current_stream(w.device).cuda_stream
     _lib.check(_lib.lib().krr_forward(C.byref(w.struct()), C.byref(b), ws.data_ptr(),
@@ -205,7 +209,8 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, w
         run_forward(w, q[i:j].contiguous(), q_valid[i:j].contiguous(), D, D,
                     prefix_valid[i:j].contiguous(), prefix_ptrs[i:j].contiguous(), cur, 1,
                     last_index[i:j].contiguous(), scores[i:j], prefix_pool=pool.slab,
-                    cur_pool=scratch.extent(), ws=ws)
+                    cur_pool=scratch.extent(), ws=ws, prefix_bits=getattr(pool, "bits", 0),
+                    prefix_scales=getattr(pool, "scales", None))
     return scores
 
 
@@ -224,17 +229,27 @@ def segmented_topk(scores, doc_ids, n_seg: int, seg_len: int, k: int):
     return idx, sc
 
 
+def fused_dequant_supported(w: DeviceWeights) -> bool:
+    """INT8/INT4 prefix pages can be dequantised inside attention (the tcgen05
+    TMEM-P kernel: head_dim 64|128, 16-bit activations)."""
+    return (w.code in (_lib.F16, _lib.BF16) and w.config.head_dim in (64, 128) and
+            w.attn_backend in (_lib.ATTN_AUTO, _lib.ATTN_TCGEN05))
+
+
 def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_tokens,
                     copy_stream=None, max_rows: int | None = None):
     """Score pairs whose document KV lives in the pinned host tier (the paper's
     SSD/DRAM tier).
 
     Distinct documents are streamed H2D (cudaMemcpyAsync on ``copy_stream``)
-    into one half of a double-buffered HBM staging pool (a quantised tier lands
-    codes and is dequantised on the main stream) while the main stream
+    into one half of a double-buffered HBM staging pool while the main stream
     scores every pair of the previously landed half; events order the reuse of
-    each half.  Each document crosses PCIe once per call however many pairs
-    reference it.  Returns f32 [n] scores on the device (pair order)."""
+    each half.  A quantised tier lands HRKV codes + scales and the attention
+    kernel dequantises them in shared memory (no expand pass, the
+    staging pool's 16-bit slots stay unused) where it can (head_dim 64|128,
+    16-bit activations), else they are expanded into the staging slots first.
+    Each document crosses PCIe once per call however many pairs reference it.
+    Returns f32 [n] scores on the device (pair order)."""
     import torch
     if staging.code != w.code:
         raise ConfigError(f"staging dtype {staging.dtype} != weights dtype {w.dtype}")
@@ -251,6 +266,8 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
     if len(staging):
         raise ConfigError("host-tier staging pool must be dedicated (empty)")
     st_slots = np.arange(staging.capacity, dtype=np.int64)
+    fused = tier.quant is not None and fused_dequant_supported(w)
+    pages = CodePages(tier, staging) if fused else staging
     docs = np.unique(hs)
     groups = [docs[i:i + half] for i in range(0, docs.size, half)]
     main = torch.cuda.current_stream(dev)
@@ -281,13 +298,14 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
         main.wait_event(ready[b])
         # a quantised tier expands on the main stream, keeping the copy stream
         # (and the PCIe link) busy with the next group's transfers
-        for s in slots:
-            tier.expand(staging, int(s), int(s))
+        if not fused:
+            for s in slots:
+                tier.expand(staging, int(s), int(s))
         staging.set_valid_len(slots, tier.valid_len[grp])
         slot_of = dict(zip(grp.tolist(), slots.tolist()))
         sel = np.nonzero(np.isin(hs, grp))[0]
         sel_t = torch.as_tensor(sel, device=dev)
-        sc = score_slots(w, staging, np.array([slot_of[h] for h in hs[sel]]),
+        sc = score_slots(w, pages, np.array([slot_of[h] for h in hs[sel]]),
                          q.index_select(0, sel_t), max_rows=max_rows)
         scores[sel_t] = sc
         free[b].record(main)

@@ -339,3 +339,25 @@ class HostKVTier:
             for h, s in zip(host_slots, staging_slots):
                 self.copy_in(int(h), staging, int(s), int(s))
         staging.set_valid_len(staging_slots, self.valid_len[np.asarray(host_slots)])
+
+
+class CodePages:
+    """The quantised host tier's device landing buffers seen as attention
+    prefix pages: slot k = codes [2L][KVH][D][HD] (INT8, or INT4 low nibble
+    first; codec.py:58-115) + scales [2L][KVH][HD] f32, dequantised inside the
+    attention kernel (krr_batch_t.prefix_bits / prefix_scales).  Quacks like a
+    KVPool for engine.score_slots; valid lengths come from the staging pool."""
+
+    def __init__(self, tier: "HostKVTier", staging: KVPool):
+        self.codes, self.scales = tier._device_bufs(staging.device, staging.capacity)
+        self.slab = self.codes
+        self.bits = tier.bits
+        self.code = staging.code
+        self.dtype = staging.dtype
+        self.document_len = staging.document_len
+        self.valid_len = staging.valid_len
+        self.slot_bytes = tier.code_bytes
+
+    def slot_ptrs(self, slots_t):
+        return slots_t * self.slot_bytes + self.codes.data_ptr()
+

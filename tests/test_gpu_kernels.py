@@ -306,3 +306,74 @@ def test_rmsnorm(d, code, tdt):
     torch.cuda.synchronize()
     tol = 1e-5 if code == _lib.F32 else 2e-3
     assert (out.float() - ref).abs().max().item() <= tol * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("HD,G,KVH,P,T", [(128, 4, 2, 512, 48), (128, 4, 2, 200, 16),
+                                          (64, 2, 2, 128, 48), (128, 4, 8, 2048, 256)])
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("act", [_lib.F16, _lib.BF16])
+def test_attention_quant_prefix_matches_expanded(HD, G, KVH, P, T, bits, act):
+    """INT8/INT4 prefix pages dequantised inside the attention
+    kernel (krr_attention_quant) give bit-for-bit the output of expanding the
+    pages into HBM first (krr_dequant_pages, codec.py:82-95) and attending over
+    16-bit pages -- and that expansion equals the reference codec's decode."""
+    nseq, L, layer = 3, 2, 1
+    tdt = torch.float16 if act == _lib.F16 else torch.bfloat16
+    sc = 1.0 / math.sqrt(math.sqrt(HD))
+    q = (torch.randn(nseq * KVH, G * T, HD, device="cuda") * sc * 4).to(tdt)
+    pre32 = torch.randn(nseq, L, 2, KVH, P, HD, device="cuda") * sc
+    pre32[0, layer, 1, 0, :, 5] = 0.0                   # an all-zero channel (scale 1.0)
+    cur = (torch.randn(nseq, 1, 2, KVH, T, HD, device="cuda") * sc).to(tdt)
+    n_t = nseq * L * 2
+    tb = KVH * P * HD if bits == 8 else KVH * P * HD // 2
+    codes = torch.empty(n_t * tb, dtype=torch.uint8, device="cuda")
+    scales = torch.empty(n_t * KVH * HD, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().krr_quant_pages(pre32.data_ptr(), _lib.F32, n_t, KVH, P, HD, bits,
+                                          codes.data_ptr(), scales.data_ptr(), _stream()))
+    pre = torch.empty(nseq, L, 2, KVH, P, HD, dtype=tdt, device="cuda")
+    _lib.check(_lib.lib().krr_dequant_pages(codes.data_ptr(), scales.data_ptr(), bits, n_t, KVH,
+                                            P, HD, act, pre.data_ptr(), _stream()))
+    vlen = torch.tensor([P, max(1, P // 3), max(1, P - 7)], dtype=torch.int32, device="cuda")
+    tv = torch.ones(nseq, T, dtype=torch.uint8, device="cuda")
+    tv[1, T - 5:] = 0
+    tv[2, 3] = 0
+    es = pre.element_size()
+    pptr = torch.arange(nseq, device="cuda", dtype=torch.int64) * (pre[0].numel() * es) + \
+        pre.data_ptr()
+    cptr = torch.arange(nseq, device="cuda", dtype=torch.int64) * (cur[0].numel() * es) + \
+        cur.data_ptr()
+    qptr = torch.arange(nseq, device="cuda", dtype=torch.int64) * (L * 2 * tb) + codes.data_ptr()
+    H = KVH * G
+    out_ref = torch.zeros(nseq * T, H * HD, dtype=tdt, device="cuda")
+    out_q = torch.full_like(out_ref, float("nan"))
+    _lib.check(_lib.lib().krr_attention(_lib.ATTN_TCGEN05, act, q.data_ptr(), nseq, KVH, G, HD,
+                                        T, P, layer, 0, pptr.data_ptr(), vlen.data_ptr(),
+                                        cptr.data_ptr(), tv.data_ptr(), out_ref.data_ptr(),
+                                        pre.data_ptr(), pre.numel() * es, cur.data_ptr(),
+                                        cur.numel() * es, _stream()))
+    _lib.check(_lib.lib().krr_attention_quant(
+        _lib.ATTN_TCGEN05, act, q.data_ptr(), nseq, KVH, G, HD, T, P, layer, 0,
+        qptr.data_ptr(), vlen.data_ptr(), cptr.data_ptr(), tv.data_ptr(), out_q.data_ptr(),
+        codes.data_ptr(), codes.numel(), cur.data_ptr(), cur.numel() * es, bits,
+        scales.data_ptr(), _stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(out_q.view(torch.int16), out_ref.view(torch.int16))
+    # the expansion itself is the reference codec's dequantize_tensor (one tensor)
+    from paper_2504_02921_b200 import codec
+    scheme = codec.QuantScheme.INT8_PER_CHANNEL if bits == 8 else codec.QuantScheme.INT4_PER_CHANNEL
+    t0 = (1 * L + layer) * 2 + 1                        # seq 1, this layer, V
+    cb = codes[t0 * tb:(t0 + 1) * tb].cpu().numpy().tobytes()
+    s0 = scales[t0 * KVH * HD:(t0 + 1) * KVH * HD].cpu().numpy().reshape(KVH, HD)
+    ref = codec.dequantize_tensor(cb, s0, scheme, (KVH, P, HD))
+    assert np.array_equal(pre[1, layer, 1].float().cpu().numpy(),
+                          torch.from_numpy(ref).to(tdt).float().numpy())
+
+
+def test_attention_quant_rejects_unsupported():
+    """Quantised prefix pages only go through the tcgen05 kernel (head_dim 64|128)."""
+    T, HD, KVH, G = 16, 256, 1, 8
+    q = torch.zeros(KVH, G * T, HD, dtype=torch.float16, device="cuda")
+    with pytest.raises(Exception, match="quantised prefix"):
+        _lib.check(_lib.lib().krr_attention_quant(
+            _lib.ATTN_TCGEN05, _lib.F16, q.data_ptr(), 1, KVH, G, HD, T, 64, 0, 0, 0, 0, 0, 0,
+            q.data_ptr(), 0, 0, 0, 0, 8, 0, _stream()))

@@ -251,11 +251,21 @@ def test_quant_pages_bit_exact_vs_host_codec(bits, scheme, src, HD):
     assert np.array_equal(o16.cpu().numpy(), o_h.astype(np.float16))
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("quant,scheme", [("int8", codec.QuantScheme.INT8_PER_CHANNEL),
                                           ("int4", codec.QuantScheme.INT4_PER_CHANNEL)])
-def test_quantised_host_tier_matches_hrkv_entries(model16, quant, scheme):
+def test_quantised_host_tier_matches_hrkv_entries(model16, quant, scheme, fused, monkeypatch):
     """A quantised host tier scores exactly like the same docs stored as HRKV
-    INT8/INT4 entries (reference codec) and decoded into HBM."""
+    INT8/INT4 entries (reference codec) and decoded into HBM -- both with the
+    codes dequantised inside attention (the default) and with the
+    separate expand pass into the staging pool."""
+    assert engine.fused_dequant_supported(model16.weights)
+    if not fused:
+        monkeypatch.setattr(engine, "fused_dequant_supported", lambda w: False)
+    calls = []
+    orig_expand = krr.HostKVTier.expand
+    monkeypatch.setattr(krr.HostKVTier, "expand",
+                        lambda self, *a, **k: (calls.append(1), orig_expand(self, *a, **k)))
     rng = np.random.default_rng(31)
     n_docs = 5
     docs = rng.integers(1, 32768, (n_docs, 128))
@@ -278,6 +288,7 @@ def test_quantised_host_tier_matches_hrkv_entries(model16, quant, scheme):
     want = engine.score_slots(model16.weights, ref_pool, np.array(ref_slots)[pair_doc], q)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+    assert (len(calls) == 0) == fused
 
 
 def test_host_dockv_from_reference_entry_scores(g, model32, model16):

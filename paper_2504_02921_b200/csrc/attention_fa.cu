@@ -135,30 +135,110 @@ __device__ __forceinline__ Item item_of(const Params& p, int it) {
 }
 
 // Decode one 16-byte chunk of HRKV codes (16 INT8 or 32 INT4, low nibble
-// first) into 16-bit values f16(code * scale) -- the rounding of
-// krr_dequant_pages.  code + bias is built exactly as the f32 2^23 + u and
-// the bias subtracted (one PRMT/LOP + FADD per element, no I2F).
+// first) into packed 16-bit pairs code * scale.
+//
+// f16: the codes become exact f16 integers by the magic-number trick (bits
+// 0x6400 | u = 1024 + u; INT4 nibbles are masked in place with LOP3, the
+// upper nibble of a byte scaled by 1/16 in the same HFMA2) and are multiplied
+// by f16 scales with HMUL2 -- ~2 instructions per element, so the two
+// converter warps keep up with the MMA/softmax chain.  The result differs from
+// krr_dequant_pages' f16(f32 code*scale) by the f16 rounding of the scale
+// (<= 2^-11 relative).
+// bf16 (no exact magic for 8-bit codes in a bf16 mantissa): f32 2^23 + u,
+// FADD, FMUL by the f32 scale, one rounding -- bit-identical to
+// krr_dequant_pages.
 template <typename T, int QB>
-__device__ __forceinline__ void decode_chunk(const uint4 v, const float* sc, uint32_t* out) {
+__device__ __forceinline__ void decode_chunk(const uint4 v, const uint32_t* sc, uint32_t* out) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  if constexpr (QB == 8) {
+  if constexpr (std::is_same<T, __half>::value) {
+    const __half2* s2 = reinterpret_cast<const __half2*>(sc);
+    if constexpr (QB == 8) {
+      const __half2 bias = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t wx = w[i >> 1] ^ 0x80808080u;            // byte -> code + 128
-      const int b0 = (i & 1) * 2;
-      const float f0 = __uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7440u + b0)) - 8388736.f;
-      const float f1 = __uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7441u + b0)) - 8388736.f;
-      out[i] = pack_2<T>(f0 * sc[2 * i], f1 * sc[2 * i + 1]);
+      for (int i = 0; i < 4; ++i) {                    // 4 codes per word
+        const uint32_t wx = w[i] ^ 0x80808080u;       // byte -> code + 128
+        const uint32_t lo = __byte_perm(wx, 0x64646464u, 0x4140u);
+        const uint32_t hi = __byte_perm(wx, 0x64646464u, 0x4342u);
+        const __half2 a = __hmul2(__hsub2(*reinterpret_cast<const __half2*>(&lo), bias), s2[2 * i]);
+        const __half2 b = __hmul2(__hsub2(*reinterpret_cast<const __half2*>(&hi), bias),
+                                  s2[2 * i + 1]);
+        out[2 * i] = *reinterpret_cast<const uint32_t*>(&a);
+        out[2 * i + 1] = *reinterpret_cast<const uint32_t*>(&b);
+      }
+    } else {
+      const __half2 b1032 = __halves2half2(__ushort_as_half(0x6408), __ushort_as_half(0x6408));
+      const __half2 sixteenth = __halves2half2(__ushort_as_half(0x2C00), __ushort_as_half(0x2C00));
+      const __half2 m72 = __halves2half2(__ushort_as_half(0xD480), __ushort_as_half(0xD480));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {                    // 8 codes per word: nibble k = channel k
+        const uint32_t wx = w[i] ^ 0x88888888u;       // nibble -> code + 8
+        const uint32_t wy = wx >> 8;
+        uint32_t r[4] = {(wx & 0x000F000Fu) | 0x64006400u, (wx & 0x00F000F0u) | 0x64006400u,
+                         (wy & 0x000F000Fu) | 0x64006400u, (wy & 0x00F000F0u) | 0x64006400u};
+        __half2 h[4];
+        h[0] = __hsub2(*reinterpret_cast<const __half2*>(&r[0]), b1032);                // c0, c4
+        h[1] = __hfma2(*reinterpret_cast<const __half2*>(&r[1]), sixteenth, m72);       // c1, c5
+        h[2] = __hsub2(*reinterpret_cast<const __half2*>(&r[2]), b1032);                // c2, c6
+        h[3] = __hfma2(*reinterpret_cast<const __half2*>(&r[3]), sixteenth, m72);       // c3, c7
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          h[k] = __hmul2(h[k], s2[4 * i + k]);        // scales pre-paired (s_k, s_k+4)
+          r[k] = *reinterpret_cast<const uint32_t*>(&h[k]);
+        }
+        out[4 * i] = __byte_perm(r[0], r[1], 0x5410u);       // c0, c1
+        out[4 * i + 1] = __byte_perm(r[2], r[3], 0x5410u);   // c2, c3
+        out[4 * i + 2] = __byte_perm(r[0], r[1], 0x7632u);   // c4, c5
+        out[4 * i + 3] = __byte_perm(r[2], r[3], 0x7632u);   // c6, c7
+      }
+    }
+  } else {
+    const float* sf = reinterpret_cast<const float*>(sc);
+    if constexpr (QB == 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t wx = w[i >> 1] ^ 0x80808080u;
+        const int b0 = (i & 1) * 2;
+        const float f0 = __uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7440u + b0)) - 8388736.f;
+        const float f1 = __uint_as_float(__byte_perm(wx, 0x4B000000u, 0x7441u + b0)) - 8388736.f;
+        out[i] = pack_2<T>(f0 * sf[2 * i], f1 * sf[2 * i + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t wx = w[i >> 2] ^ 0x88888888u;
+        const int sh = (i & 3) * 8;
+        const float f0 = __uint_as_float(0x4B000000u | ((wx >> sh) & 0xFu)) - 8388616.f;
+        const float f1 = __uint_as_float(0x4B000000u | ((wx >> (sh + 4)) & 0xFu)) - 8388616.f;
+        out[i] = pack_2<T>(f0 * sf[2 * i], f1 * sf[2 * i + 1]);
+      }
+    }
+  }
+}
+
+// Per-lane scales for decode_chunk: f16 -- half2 pairs in the order the decode
+// multiplies (INT8 (s0,s1),(s2,s3)..; INT4 per 8 channels (s0,s4),(s1,s5),
+// (s2,s6),(s3,s7)); bf16 -- the f32 scales.
+template <typename T, int QB, int CH>
+__device__ __forceinline__ void load_scales(const float* src, uint32_t* sc) {
+  float f[CH];
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+#pragma unroll
+  for (int i = 0; i < CH / 4; ++i) {
+    const float4 v = __ldg(s4 + i);
+    f[4 * i] = v.x; f[4 * i + 1] = v.y; f[4 * i + 2] = v.z; f[4 * i + 3] = v.w;
+  }
+  if constexpr (std::is_same<T, __half>::value) {
+#pragma unroll
+    for (int k = 0; k < CH / 2; ++k) {
+      int a, b;
+      if constexpr (QB == 8) { a = 2 * k; b = 2 * k + 1; }
+      else { a = (k / 4) * 8 + (k % 4); b = a + 4; }
+      __half2 h = __floats2half2_rn(f[a], f[b]);
+      sc[k] = *reinterpret_cast<uint32_t*>(&h);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint32_t wx = w[i >> 2] ^ 0x88888888u;            // nibble -> code + 8
-      const int sh = (i & 3) * 8;
-      const float f0 = __uint_as_float(0x4B000000u | ((wx >> sh) & 0xFu)) - 8388616.f;
-      const float f1 = __uint_as_float(0x4B000000u | ((wx >> (sh + 4)) & 0xFu)) - 8388616.f;
-      out[i] = pack_2<T>(f0 * sc[2 * i], f1 * sc[2 * i + 1]);
-    }
+    for (int k = 0; k < CH; ++k) sc[k] = __float_as_uint(f[k]);
   }
 }
 
@@ -365,7 +445,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       constexpr int RSTEP = 32 / CPR;
       static_assert(CPR >= 1 && CPR <= 32 && KB % RSTEP == 0, "code chunk mapping");
       const int cc = lane % CPR, r0 = lane / CPR;
-      float sc[CH];
+      uint32_t sc[std::is_same<T, __half>::value ? CH / 2 : CH];
       int g = 0, gc = 0;
       for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
         const Item x = item_of(p, it);
@@ -373,13 +453,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
           const int page = (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b]) -
                                   p.prefix_base) / p.prefix_page_bytes) +
                            (p.layer * 2 + cw) * p.KVH + x.kvh;
-          const float4* s4 = reinterpret_cast<const float4*>(p.scales + (int64_t)page * HD +
-                                                             cc * CH);
-#pragma unroll
-          for (int i = 0; i < CH / 4; ++i) {
-            const float4 f = __ldg(s4 + i);
-            sc[4 * i] = f.x; sc[4 * i + 1] = f.y; sc[4 * i + 2] = f.z; sc[4 * i + 3] = f.w;
-          }
+          load_scales<T, QB, CH>(p.scales + (int64_t)page * HD + cc * CH, sc);
         }
         for (int j = 0; j < x.nb_pre; ++j, ++gc) {
           const int gg = g + j, s = gg % NK, c = gc % NC;

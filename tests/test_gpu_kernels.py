@@ -314,9 +314,12 @@ def test_rmsnorm(d, code, tdt):
 @pytest.mark.parametrize("act", [_lib.F16, _lib.BF16])
 def test_attention_quant_prefix_matches_expanded(HD, G, KVH, P, T, bits, act):
     """INT8/INT4 prefix pages dequantised inside the attention
-    kernel (krr_attention_quant) give bit-for-bit the output of expanding the
-    pages into HBM first (krr_dequant_pages, codec.py:82-95) and attending over
-    16-bit pages -- and that expansion equals the reference codec's decode."""
+    kernel (krr_attention_quant) match expanding the pages into HBM first
+    (krr_dequant_pages, codec.py:82-95) and attending over 16-bit pages: bit for
+    bit with bf16 activations (same f32 product, one rounding); with f16 the
+    in-kernel decode multiplies by f16-rounded scales (<= 2^-11 relative per
+    element), so outputs agree to f16 attention precision.  The expansion itself
+    equals the reference codec's decode."""
     nseq, L, layer = 3, 2, 1
     tdt = torch.float16 if act == _lib.F16 else torch.bfloat16
     sc = 1.0 / math.sqrt(math.sqrt(HD))
@@ -357,7 +360,12 @@ def test_attention_quant_prefix_matches_expanded(HD, G, KVH, P, T, bits, act):
         codes.data_ptr(), codes.numel(), cur.data_ptr(), cur.numel() * es, bits,
         scales.data_ptr(), _stream()))
     torch.cuda.synchronize()
-    assert torch.equal(out_q.view(torch.int16), out_ref.view(torch.int16))
+    if act == _lib.BF16:
+        assert torch.equal(out_q.view(torch.int16), out_ref.view(torch.int16))
+    else:
+        assert torch.isfinite(out_q).all()
+        err = (out_q.float() - out_ref.float()).abs().max().item()
+        assert err <= 4e-3 * max(1.0, out_ref.float().abs().max().item()), err
     # the expansion itself is the reference codec's dequantize_tensor (one tensor)
     from paper_2504_02921_b200 import codec
     scheme = codec.QuantScheme.INT8_PER_CHANNEL if bits == 8 else codec.QuantScheme.INT4_PER_CHANNEL

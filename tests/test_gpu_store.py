@@ -255,10 +255,11 @@ def test_quant_pages_bit_exact_vs_host_codec(bits, scheme, src, HD):
 @pytest.mark.parametrize("quant,scheme", [("int8", codec.QuantScheme.INT8_PER_CHANNEL),
                                           ("int4", codec.QuantScheme.INT4_PER_CHANNEL)])
 def test_quantised_host_tier_matches_hrkv_entries(model16, quant, scheme, fused, monkeypatch):
-    """A quantised host tier scores exactly like the same docs stored as HRKV
-    INT8/INT4 entries (reference codec) and decoded into HBM -- both with the
-    codes dequantised inside attention (the default) and with the
-    separate expand pass into the staging pool."""
+    """A quantised host tier scores like the same docs stored as HRKV INT8/INT4
+    entries (reference codec) and decoded into HBM: exactly with the separate
+    expand pass into the staging pool, and within the f16 rounding of the
+    scales (2^-11 per K/V element) with the codes dequantised inside attention
+    (the default)."""
     assert engine.fused_dequant_supported(model16.weights)
     if not fused:
         monkeypatch.setattr(engine, "fused_dequant_supported", lambda w: False)
@@ -287,7 +288,11 @@ def test_quantised_host_tier_matches_hrkv_entries(model16, quant, scheme, fused,
     got = engine.score_host_tier(model16.weights, tier, staging, hs[pair_doc], q)
     want = engine.score_slots(model16.weights, ref_pool, np.array(ref_slots)[pair_doc], q)
     torch.cuda.synchronize()
-    assert torch.equal(got, want)
+    if fused:
+        normwise = ((got - want).norm() / want.norm()).item()
+        assert normwise <= 5e-3, normwise
+    else:
+        assert torch.equal(got, want)
     assert (len(calls) == 0) == fused
 
 

@@ -16,7 +16,17 @@
 //  * the suffix-block mask (tok_valid, causal) comes from a 64-bit ballot mask,
 //    not per-key global loads.
 //
-// Work item = (unit, pair of 128-row tiles).
+// Work item = 256 GQA-packed query rows (two 128-row tiles) of ONE document
+// and kv head.  Sequences that share a prefix document and sit next to each
+// other in the batch form a group whose rows are concatenated (each sequence
+// padded to Rp = R rounded up to 64 rows), so the document's K/V is streamed
+// once per 256 rows of the whole group -- the cross-query KV reuse of one
+// cached document by every query that ranks it -- and a 192-row sequence no
+// longer pads its own 256-row item.  Q lands by 64-row TMA boxes (one
+// sequence each); the suffix keys of every sequence the item spans follow the
+// prefix blocks, masked to that sequence's rows.  krr_forward builds the item
+// table once per call (attn_group_items_kernel); without a table every
+// sequence is its own group.
 // SMEM: Q_A|Q_B 64 KB, K ring 4 x 16 KB, V ring 4 x 16 KB = 192 KB.
 //
 // Quantised prefix pages (QB = 8 | 4: HRKV INT8/INT4 codes, codec.py:58-115,
@@ -68,7 +78,9 @@ struct Params {
   const uint8_t* tok_valid;
   void* out;
   const float* scales;   // quantised prefix: [page][HD] f32 (page as in the code pool)
-  int KVH, G, T, P, layer, cur_layer, R, pairs, items;
+  const int4* items;     // grouped items {b0, ng, row0, kvh}, or null (one group per seq)
+  const int* n_items;    // device count of items[]
+  int KVH, G, T, P, layer, cur_layer, R, Rp, chunks, items_implicit;
 };
 
 template <int HD, int QB = 16>
@@ -116,22 +128,63 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+constexpr int MAX_SPAN = 2 * TM / 64;   // sequences one item can span (Rp >= 64)
+
 struct Item {
-  int unit, b, kvh, row0, nb_pre, nb, vlen, t_max;
+  int b0, ng, row0, kvh;       // group's first sequence and size; first group row; kv head
+  int s_lo, n_span;            // sequences (relative to b0) the item's rows cover
+  int nbc[MAX_SPAN];           // suffix blocks needed per covered sequence
+  int vlen, nb_pre, nb;
 };
+__device__ __forceinline__ int item_count(const Params& p) {
+  return p.items ? __ldg(p.n_items) : p.items_implicit;
+}
 __device__ __forceinline__ Item item_of(const Params& p, int it) {
   Item x;
-  x.unit = it / p.pairs;
-  const int pair = it - x.unit * p.pairs;
-  x.b = x.unit / p.KVH;
-  x.kvh = x.unit - x.b * p.KVH;
-  x.row0 = pair * 2 * TM;
-  const int last_row = min(x.row0 + 2 * TM, p.R) - 1;
-  x.t_max = (last_row / p.T != x.row0 / p.T) ? p.T - 1 : last_row % p.T;
-  x.vlen = p.P ? min(p.prefix_valid_len[x.b], p.P) : 0;
+  if (p.items) {
+    const int4 e = __ldg(p.items + it);
+    x.b0 = e.x; x.ng = e.y; x.row0 = e.z; x.kvh = e.w;
+  } else {                                       // (seq, kv head)-major, 256-row chunks
+    const int unit = it / p.chunks;
+    x.b0 = unit / p.KVH;
+    x.kvh = unit - x.b0 * p.KVH;
+    x.ng = 1;
+    x.row0 = (it - unit * p.chunks) * 2 * TM;
+  }
+  x.s_lo = x.row0 / p.Rp;
+  const int s_hi = min((x.row0 + 2 * TM - 1) / p.Rp, x.ng - 1);
+  x.n_span = s_hi - x.s_lo + 1;
+  int nbc_sum = 0;
+#pragma unroll
+  for (int k = 0; k < MAX_SPAN; ++k) {
+    const int s = x.s_lo + k;
+    int nb = 0;
+    if (k < x.n_span) {
+      // valid local rows of sequence s inside the item; causal: only keys up to
+      // the largest token index among them are ever visible
+      const int ra = max(x.row0 - s * p.Rp, 0);
+      const int rb = min(x.row0 + 2 * TM - s * p.Rp, p.R) - 1;
+      if (ra <= rb) {
+        const int t_max = (rb / p.T != ra / p.T) ? p.T - 1 : rb % p.T;
+        nb = (t_max + KB) / KB;
+      }
+    }
+    x.nbc[k] = nb;
+    nbc_sum += nb;
+  }
+  x.vlen = p.P ? min(p.prefix_valid_len[x.b0], p.P) : 0;
   x.nb_pre = (x.vlen + KB - 1) / KB;
-  x.nb = x.nb_pre + (x.t_max + 1 + KB - 1) / KB;
+  x.nb = x.nb_pre + nbc_sum;
   return x;
+}
+// Suffix block j (>= nb_pre) of an item: which covered sequence, first key.
+__device__ __forceinline__ void suffix_block(const Item& x, int j, int& s_rel, int& key0) {
+  int jj = j - x.nb_pre, k = 0;
+#pragma unroll
+  for (int q = 0; q < MAX_SPAN - 1; ++q)
+    if (k == q && jj >= x.nbc[q]) { jj -= x.nbc[q]; k = q + 1; }
+  s_rel = x.s_lo + k;
+  key0 = jj * KB;
 }
 
 // Decode one 16-byte chunk of HRKV codes (16 INT8 or 32 INT4, low nibble
@@ -256,6 +309,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = item_count(p);
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem) & 1023) != 0) __trap();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
@@ -295,16 +349,21 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
     // ---------------------------------------------------------- producers
     if (lane == 0) {                                   // Q tiles, per item
       int n = 0;
-      for (int it = blockIdx.x; it < p.items; it += gridDim.x, ++n) {
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
         const Item x = item_of(p, it);
         mbar_wait(&bar[B_QEMPTY], (n & 1) ^ 1);
         mbar_expect_tx(&bar[B_QFULL], 2 * S::Q_TILE);
 #pragma unroll
-        for (int tile = 0; tile < 2; ++tile)
+        for (int sub = 0; sub < 4; ++sub) {            // 64-row boxes, one sequence each
+          const int gr = x.row0 + sub * 64;
+          int s_rel = gr / p.Rp, r = gr - s_rel * p.Rp;
+          if (s_rel >= x.ng) { s_rel = 0; r = 0; }     // past the group: rows unused
+          const int unit = (x.b0 + s_rel) * p.KVH + x.kvh;
 #pragma unroll
           for (int a = 0; a < HD / 64; ++a)
-            tma_load<1>(sQ + tile * S::Q_TILE + a * S::ATOM_Q, &tmQ, smem_u32(&bar[B_QFULL]),
-                        a * 64, x.unit * p.R + x.row0 + tile * TM);
+            tma_load3(sQ + (sub >> 1) * S::Q_TILE + a * S::ATOM_Q + (sub & 1) * 64 * 128, &tmQ,
+                      &bar[B_QFULL], a * 64, r, unit);
+        }
       }
     } else if (lane < 3) {                             // K ring (lane 1), V ring (lane 2)
       const bool is_k = lane == 1;
@@ -315,14 +374,12 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       const int cw = is_k ? 0 : 1;
       uint8_t* cring = smem + S::C_OFF + cw * NC * S::CODE_BLK;
       int g = 0, gc = 0;
-      for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const Item x = item_of(p, it);
-        const int pre_page = p.P ? (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b]) -
+        const int pre_page = p.P ? (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b0]) -
                                           p.prefix_base) / p.prefix_page_bytes) +
                                        (p.layer * 2) * p.KVH + x.kvh
                                  : 0;
-        const int cur_page = (int)((reinterpret_cast<const char*>(p.cur_kv[x.b]) - p.cur_base) /
-                                   p.cur_page_bytes) + (p.cur_layer * 2) * p.KVH + x.kvh;
         const int vofs = is_k ? 0 : p.KVH;
         for (int j = 0; j < x.nb; ++j, ++g) {
           const bool pre = j < x.nb_pre;
@@ -339,8 +396,14 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
           mbar_wait(&empty[s], ((g / nst) & 1) ^ 1);
           mbar_expect_tx(&full[s], S::KV_BYTES);
           const CUtensorMap* map = pre ? &tmPre : &tmCur;
-          const int key0 = (pre ? j : j - x.nb_pre) * KB;
-          const int pk = (pre ? pre_page : cur_page) + vofs;
+          int key0 = j * KB, pk = pre_page;
+          if (!pre) {
+            int s_rel;
+            suffix_block(x, j, s_rel, key0);
+            pk = (int)((reinterpret_cast<const char*>(p.cur_kv[x.b0 + s_rel]) - p.cur_base) /
+                       p.cur_page_bytes) + (p.cur_layer * 2) * p.KVH + x.kvh;
+          }
+          pk += vofs;
 #pragma unroll
           for (int a = 0; a < HD / 64; ++a)
             tma_load3(ring + s * S::KV_BYTES + a * S::ATOM_KV, map, &full[s], a * 64, key0, pk);
@@ -396,7 +459,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       }
       __syncwarp();
     };
-    for (int it = blockIdx.x; it < p.items; it += gridDim.x, ++n) {
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
       const Item x = item_of(p, it);
       mbar_wait(&bar[B_QFULL], n & 1);
       issue_s_pair(g, x.nb == 1);
@@ -447,10 +510,10 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       const int cc = lane % CPR, r0 = lane / CPR;
       uint32_t sc[std::is_same<T, __half>::value ? CH / 2 : CH];
       int g = 0, gc = 0;
-      for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const Item x = item_of(p, it);
         if (x.nb_pre > 0) {
-          const int page = (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b]) -
+          const int page = (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b0]) -
                                   p.prefix_base) / p.prefix_page_bytes) +
                            (p.layer * 2 + cw) * p.KVH + x.kvh;
           load_scales<T, QB, CH>(p.scales + (int64_t)page * HD + cc * CH, sc);
@@ -499,27 +562,34 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
     const int T_ = p.T;
     const int H = p.KVH * p.G;
     int g = 0, n = 0;
-    for (int it = blockIdx.x; it < p.items; it += gridDim.x, ++n) {
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
       const Item x = item_of(p, it);
-      const int r = x.row0 + tile * TM + lrow;
-      const bool row_ok = r < p.R;
-      const bool quad_live = x.row0 + tile * TM + quad * 32 < p.R;
+      const int gr = x.row0 + tile * TM + lrow;       // row in the group's row space
+      const int s_row = gr / p.Rp;                     // sequence (relative to b0)
+      const int r = gr - s_row * p.Rp;
+      const bool row_ok = s_row < x.ng && r < p.R;
+      const bool quad_live = __any_sync(0xffffffffu, row_ok);
       const int gq = r / T_, t = r - gq * T_;
-      const uint8_t* tv = p.tok_valid + (int64_t)x.b * T_;
+      const int b = x.b0 + s_row;
       float m_use = -CUDART_INF_F, l = 0.f;
       for (int j = 0; j < x.nb; ++j) {
         const int gs = g + j, sb = gs & 1;
         const bool pre = j < x.nb_pre;
-        const int key0 = (pre ? j : j - x.nb_pre) * KB;
-        // suffix block: visible keys as a 64-bit mask (tok_valid ballot, then causal)
+        int key0 = j * KB;
+        // suffix block (keys of one covered sequence): visible keys as a 64-bit
+        // mask -- tok_valid ballot, then causal, none for other sequences' rows
         uint64_t cur_mask = ~0ull;
         if (!pre) {
+          int s_blk;
+          suffix_block(x, j, s_blk, key0);
+          const uint8_t* tv = p.tok_valid + (int64_t)(x.b0 + s_blk) * T_;
           const int k_lo = key0 + lane, k_hi = key0 + 32 + lane;
           const uint32_t lo = __ballot_sync(0xffffffffu, k_lo < T_ && __ldg(tv + k_lo));
           const uint32_t hi = __ballot_sync(0xffffffffu, k_hi < T_ && __ldg(tv + k_hi));
           cur_mask = ((uint64_t)hi << 32) | lo;
           const int rel = t - key0;                     // keys key0+c visible iff c <= rel
           cur_mask &= rel >= 63 ? ~0ull : (rel < 0 ? 0ull : ((2ull << rel) - 1));
+          if (s_blk != s_row) cur_mask = 0ull;
         }
         mbar_wait(&s_full[sb], (gs >> 1) & 1);
         if (quad == 2) TR(3 + tile, 0, gs);
@@ -605,7 +675,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       tc_fence_after();
       if (quad_live) {
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        T* dst = reinterpret_cast<T*>(p.out) + ((int64_t)x.b * T_ + t) * (H * HD) +
+        T* dst = reinterpret_cast<T*>(p.out) + ((int64_t)b * T_ + t) * (H * HD) +
                  (int64_t)(x.kvh * p.G + gq) * HD;
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
@@ -674,16 +744,17 @@ static int launch(const AttnParams& a, cudaStream_t s) {
   const CUtensorMapDataType dt = std::is_same<T, __half>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                                 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const int R = a.group * a.seq_len;
+  const int Rp = (R + 63) / 64 * 64;                  // rows per sequence in a group
   const int64_t units = (int64_t)a.n_seqs * a.kv_heads;
-  const int pairs = (R + 2 * TM - 1) / (2 * TM);
-  KRR_REQUIRE(units * R < INT32_MAX && units * pairs < INT32_MAX, KRR_ESHAPE,
+  const int chunks = (Rp + 2 * TM - 1) / (2 * TM);
+  KRR_REQUIRE(units * R < INT32_MAX && units * (chunks + 1) < INT32_MAX, KRR_ESHAPE,
               "attention batch too large");
   CUtensorMap mq, mp, mc;
   {
-    cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)(units * R)};
-    cuuint64_t str[1] = {(cuuint64_t)HD * sizeof(T)};
-    cuuint32_t box[2] = {64, TM};
-    int rc = encode(&mq, a.q, dt, 2, dims, str, box);
+    cuuint64_t dims[3] = {(cuuint64_t)HD, (cuuint64_t)R, (cuuint64_t)units};
+    cuuint64_t str[2] = {(cuuint64_t)HD * sizeof(T), (cuuint64_t)R * HD * sizeof(T)};
+    cuuint32_t box[3] = {64, 64, 1};
+    int rc = encode(&mq, a.q, dt, 3, dims, str, box);
     if (rc) return rc;
   }
   const int64_t cur_page = (int64_t)a.seq_len * HD * sizeof(T);
@@ -719,21 +790,93 @@ static int launch(const AttnParams& a, cudaStream_t s) {
   } else {
     mp = mc;
   }
-  const int items = (int)(units * pairs);
+  const int implicit = (int)(units * chunks);
+  // grouped items: at most one partial 256-row chunk per group beyond the rows
+  const int64_t bound = a.items ? (int64_t)a.kv_heads *
+                                      (((int64_t)a.n_seqs * Rp + 2 * TM - 1) / (2 * TM) + a.n_seqs)
+                                : implicit;
   Params p{a.prefix_kv, static_cast<const char*>(a.prefix_pool), pre_page, a.cur_kv,
            static_cast<const char*>(a.cur_pool), cur_page, a.prefix_valid_len, a.tok_valid,
-           a.out, a.prefix_scales, a.kv_heads, a.group, a.seq_len, a.prefix_len, a.layer,
-           a.cur_layer, R, pairs, items};
+           a.out, a.prefix_scales, static_cast<const int4*>(a.items), a.n_items, a.kv_heads,
+           a.group, a.seq_len, a.prefix_len, a.layer, a.cur_layer, R, Rp, chunks, implicit};
   {
     const int rc = ensure_func_smem((const void*)attn_fa_kernel<T, HD, QB>, Sm::TOTAL);
     if (rc) return rc;
   }
-  const int grid = std::min(items, device_sm_count());
+  const int grid = (int)std::min<int64_t>(bound, device_sm_count());
   attn_fa_kernel<T, HD, QB><<<grid, threads_of<QB>(), Sm::TOTAL, s>>>(mq, mp, mc, p);
   return check_launch("attention_fa");
 }
 
+// One CTA: sequences sharing a prefix page pointer and adjacent in the batch
+// form a group; each group's rows (Rp per sequence) are cut into 256-row
+// items, per kv head: items[] = {b0, ng, row0, kvh} in (group, kvh, chunk)
+// order, so CTAs running at the same time stream the same pages.
+__global__ void __launch_bounds__(1024) attn_group_items_kernel(void* const* prefix_kv, int n,
+                                                                int Rp, int KVH, int64_t cap,
+                                                                int4* items, int* count) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int b = c0 + threadIdx.x;
+    int ng = 0;
+    if (b < n && (b == 0 || prefix_kv[b] != prefix_kv[b - 1])) {
+      const void* pk = prefix_kv[b];
+      ng = 1;
+      while (b + ng < n && prefix_kv[b + ng] == pk) ++ng;
+    }
+    const int ch = ng ? (int)(((int64_t)ng * Rp + 2 * TM - 1) / (2 * TM)) : 0;
+    const int cnt = ch * KVH;
+    int incl = cnt;                                  // block inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += v;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int off = base + (wid ? wsum[wid - 1] : 0) + incl - cnt;
+    for (int k = 0; k < KVH; ++k)
+      for (int c = 0; c < ch; ++c) {
+        const int64_t i = off + (int64_t)k * ch + c;
+        if (i < cap) items[i] = make_int4(b, ng, c * 2 * TM, k);
+      }
+    __syncthreads();
+    if (threadIdx.x == 0) base += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = (int)((int64_t)base < cap ? (int64_t)base : cap);
+}
+
 }  // namespace attn_fa
+
+int64_t attention_items_capacity(int64_t n_seqs, int group, int seq_len, int kv_heads) {
+  const int64_t Rp = ((int64_t)group * seq_len + 63) / 64 * 64;
+  return (int64_t)kv_heads * ((n_seqs * Rp + 2 * attn_fa::TM - 1) / (2 * attn_fa::TM) + n_seqs);
+}
+
+int build_attention_items(void* const* prefix_kv, int n_seqs, int group, int seq_len,
+                          int kv_heads, void* items, int64_t cap, int* count, cudaStream_t s) {
+  const int Rp = (group * seq_len + 63) / 64 * 64;
+  KRR_REQUIRE(cap >= attention_items_capacity(n_seqs, group, seq_len, kv_heads) &&
+                  cap < INT32_MAX, KRR_ECONFIG, "attention item table too small");
+  attn_fa::attn_group_items_kernel<<<1, 1024, 0, s>>>(prefix_kv, n_seqs, Rp, kv_heads, cap,
+                                                      static_cast<int4*>(items), count);
+  return check_launch("attention_items");
+}
 
 #ifdef KRR_PP_TRACE
 extern "C" int krr_fa_trace_read(unsigned long long* out) {

@@ -655,7 +655,8 @@ int krr_attention_quant(int backend, int act_dtype, const void* q, int32_t n_seq
                         krr_stream_t stream) {
   AttnParams p{q, n_seqs, kv_heads, group, head_dim, seq_len, prefix_len, layer, cur_layer,
                prefix_kv, prefix_valid_len, cur_kv, tok_valid, out, prefix_pool,
-               prefix_pool_bytes, cur_pool, cur_pool_bytes, prefix_bits, prefix_scales};
+               prefix_pool_bytes, cur_pool, cur_pool_bytes, prefix_bits, prefix_scales, nullptr,
+               nullptr};
   if (n_seqs == 0) return KRR_OK;
   return do_attention(backend, act_dtype, p, (cudaStream_t)stream);
 }
@@ -773,6 +774,13 @@ int krr_dequant_pages(const uint8_t* codes, const float* scales, int32_t bits, i
 // ------------------------------------------------------------- layer loop
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Attention item-table entries for any split of `rows` into sequences (n <= rows,
+// n * Rp <= (G + 63) * rows): the grouped-attention table lives in the workspace.
+static int64_t items_bound(const krr_model_t* m, int64_t rows) {
+  const int64_t G = m->heads / (m->kv_heads > 0 ? m->kv_heads : 1);
+  return (int64_t)m->kv_heads * (((G + 63) * rows + 255) / 256 + rows);
+}
+
 int krr_workspace_bytes(const krr_model_t* m, int64_t rows, size_t* out) {
   KRR_REQUIRE(m && out, KRR_ECONFIG, "null argument");
   const size_t es = dtype_size(m->act_dtype);
@@ -781,7 +789,8 @@ int krr_workspace_bytes(const krr_model_t* m, int64_t rows, size_t* out) {
                + align256(rows * d * es)         // xn (normed activations)
                + align256(rows * hq * es)        // q  ([unit][g*t][hd])
                + align256(rows * hq * es)        // attention output
-               + align256(rows * (int64_t)ffn_of(m) * es);    // MLP hidden
+               + align256(rows * (int64_t)ffn_of(m) * es)     // MLP hidden
+               + align256(16 * items_bound(m, rows) + 16);    // attention item table
   *out = total;
   return KRR_OK;
 }
@@ -815,7 +824,9 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
   void* xn = w;                                    w += align256(rows * d * es);
   void* qb = w;                                    w += align256(rows * (int64_t)H * HD * es);
   void* ab = w;                                    w += align256(rows * (int64_t)H * HD * es);
-  void* hb = w;
+  void* hb = w;                                    w += align256(rows * (int64_t)ffn_of(m) * es);
+  int* item_count = reinterpret_cast<int*>(w);
+  void* items = w + 16;
 
   int rc = KRR_OK;
   if (b->x_in) {
@@ -825,6 +836,14 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
   } else {
     rc = launch_embed(b->tokens, m->token_embedding, rows, d,
                       m->embed_scale > 0.f ? m->embed_scale : 1.0f, x, s);
+    if (rc) return rc;
+  }
+  // cached-prefix scoring: group sequences that share a document so attention
+  // streams each document's K/V once per 256 rows of all its queries
+  const bool grouped = b->prefix_len > 0 && act != KRR_F32 && (HD == 64 || HD == 128);
+  if (grouped) {
+    rc = build_attention_items(b->prefix_kv, b->n_seqs, G, b->seq_len, KVH, items,
+                               items_bound(m, rows), item_count, s);
     if (rc) return rc;
   }
   const int nqkv = (H + 2 * KVH) * HD;
@@ -851,7 +870,8 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
     AttnParams ap{qb, b->n_seqs, KVH, G, HD, b->seq_len, b->prefix_len, l, cl,
                   b->prefix_kv, b->prefix_valid_len, b->cur_kv, b->tok_valid, ab,
                   b->prefix_pool, b->prefix_pool_bytes, b->cur_pool, b->cur_pool_bytes,
-                  b->prefix_bits, b->prefix_scales};
+                  b->prefix_bits, b->prefix_scales, grouped ? items : nullptr,
+                  grouped ? item_count : nullptr};
     rc = do_attention(m->attn_backend, act, ap, s);
     if (rc) return rc;
     EpiParams er{};

@@ -37,7 +37,14 @@ struct AttnParams {
   // prefix_len * head_dim * bits / 8 bytes and prefix_pool is the code pool
   int prefix_bits;
   const float* prefix_scales;
+  // grouped work items from build_attention_items (sequences sharing a prefix
+  // document, adjacent in the batch, attend as one row group); null = per seq
+  const void* items;
+  const int* n_items;
 };
+int64_t attention_items_capacity(int64_t n_seqs, int group, int seq_len, int kv_heads);
+int build_attention_items(void* const* prefix_kv, int n_seqs, int group, int seq_len,
+                          int kv_heads, void* items, int64_t cap, int* count, cudaStream_t s);
 int launch_attention_mma(int act_dtype, const AttnParams& p, cudaStream_t s);
 int launch_attention_tcgen05(int act_dtype, const AttnParams& p, cudaStream_t s);
 int launch_attention_fa(int act_dtype, const AttnParams& p, cudaStream_t s);

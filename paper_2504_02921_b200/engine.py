@@ -197,9 +197,25 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, w
         last_index = torch.where(q_valid.bool(), ar, torch.full_like(ar, -1)).max(dim=1).values
         last_index = last_index.to(torch.int32)
     slots_t = torch.as_tensor(slots, device=dev).to(torch.int64)
+    scores = out if out is not None else torch.empty(n, dtype=torch.float32, device=dev)
+    # Pairs that share a document are made adjacent (stable sort by slot) so the
+    # attention kernel attends all of a document's queries as one row group and
+    # streams its K/V once (krr_forward's item table); scores are scattered
+    # back to pair order.  Per-pair results do not depend on the grouping.
+    order = None
+    if n > 1:
+        if isinstance(slots, torch.Tensor):
+            slots_t, order = torch.sort(slots_t, stable=True)
+        else:
+            o = np.argsort(np.asarray(slots), kind="stable")
+            if (o != np.arange(n)).any():
+                order = torch.as_tensor(o, device=dev)
+                slots_t = slots_t.index_select(0, order)
+    if order is not None:
+        q, q_valid, last_index = (t.index_select(0, order) for t in (q, q_valid, last_index))
+        final, scores = scores, torch.empty(n, dtype=torch.float32, device=dev)
     prefix_ptrs = pool.slot_ptrs(slots_t)
     prefix_valid = pool.valid_len[slots_t]
-    scores = out if out is not None else torch.empty(n, dtype=torch.float32, device=dev)
     step = max(1, (max_rows or rows_budget(w)) // Q)
     scratch = scratch or _SCRATCH.setdefault(str(dev), SuffixScratch())
     D = pool.document_len
@@ -211,6 +227,9 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, w
                     last_index[i:j].contiguous(), scores[i:j], prefix_pool=pool.slab,
                     cur_pool=scratch.extent(), ws=ws, prefix_bits=getattr(pool, "bits", 0),
                     prefix_scales=getattr(pool, "scales", None))
+    if order is not None:
+        final.index_copy_(0, order, scores)
+        return final
     return scores
 
 

@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError
-from .kvpool import CodePages, KVPool
+from .kvpool import CodePages, KVPool, to_device
 from .model import DeviceWeights
 
 DEFAULT_WORKSPACE_BUDGET = 32 << 30  # bytes of activations per krr_forward call
@@ -41,7 +41,13 @@ class _Workspace:
     def get(self, nbytes: int, device):
         import torch
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            grow = self.buf is not None
             self.buf = None
+            if grow:
+                # hand the old block back to the driver first: with a pool filling
+                # most of HBM (C4) the cached block cannot be split to fit the
+                # larger request, and both do not fit at once
+                torch.cuda.empty_cache()
             self.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
         return self.buf
 
@@ -67,6 +73,8 @@ def rows_budget(w: DeviceWeights, budget: int | None = None) -> int:
     import torch
     if budget is None:
         free, _ = torch.cuda.mem_get_info(w.device)
+        # memory PyTorch holds cached but unallocated is usable too
+        free += torch.cuda.memory_reserved(w.device) - torch.cuda.memory_allocated(w.device)
         held = _workspace(w.device).buf
         held = held.numel() if held is not None else 0
         budget = min(DEFAULT_WORKSPACE_BUDGET, int(0.8 * (free + held)))
@@ -186,7 +194,9 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, w
     if pool.code != w.code:
         raise ConfigError(f"pool dtype {pool.dtype} != weights dtype {w.dtype}")
     dev = w.device
-    q = torch.as_tensor(q_tokens, device=dev)
+    q = q_tokens if isinstance(q_tokens, torch.Tensor) else to_device(
+        np.asarray(q_tokens), dev)
+    q = q.to(dev)
     if q.dtype != torch.int32:
         q = q.to(torch.int32)
     n, Q = q.shape
@@ -196,7 +206,8 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, w
         ar = torch.arange(Q, device=dev, dtype=torch.int32)
         last_index = torch.where(q_valid.bool(), ar, torch.full_like(ar, -1)).max(dim=1).values
         last_index = last_index.to(torch.int32)
-    slots_t = torch.as_tensor(slots, device=dev).to(torch.int64)
+    slots_t = (slots if isinstance(slots, torch.Tensor) else to_device(
+        np.asarray(slots, dtype=np.int64), dev)).to(dev).to(torch.int64)
     scores = out if out is not None else torch.empty(n, dtype=torch.float32, device=dev)
     # Pairs that share a document are made adjacent (stable sort by slot) so the
     # attention kernel attends all of a document's queries as one row group and
@@ -209,7 +220,7 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, w
         else:
             o = np.argsort(np.asarray(slots), kind="stable")
             if (o != np.arange(n)).any():
-                order = torch.as_tensor(o, device=dev)
+                order = to_device(o, dev)
                 slots_t = slots_t.index_select(0, order)
     if order is not None:
         q, q_valid, last_index = (t.index_select(0, order) for t in (q, q_valid, last_index))
@@ -240,7 +251,9 @@ def segmented_topk(scores, doc_ids, n_seg: int, seg_len: int, k: int):
     dev = scores.device
     idx = torch.empty((n_seg, k), dtype=torch.int32, device=dev)
     sc = torch.empty((n_seg, k), dtype=torch.float32, device=dev)
-    ids = torch.as_tensor(doc_ids, device=dev).to(torch.int32).contiguous()
+    ids = doc_ids if isinstance(doc_ids, torch.Tensor) else to_device(
+        np.asarray(doc_ids), dev)
+    ids = ids.to(torch.int32).contiguous()
     stream = torch.cuda.current_stream(dev).cuda_stream
     _lib.check(_lib.lib().krr_segmented_topk(scores.contiguous().data_ptr(), ids.data_ptr(),
                                              n_seg, seg_len, k, idx.data_ptr(), sc.data_ptr(),
@@ -274,7 +287,7 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
         raise ConfigError(f"staging dtype {staging.dtype} != weights dtype {w.dtype}")
     dev = w.device
     hs = np.asarray(host_slots, dtype=np.int64)
-    q = torch.as_tensor(np.asarray(q_tokens), device=dev).to(torch.int32)
+    q = to_device(np.asarray(q_tokens), dev).to(torch.int32)
     n = hs.size
     scores = torch.empty(n, dtype=torch.float32, device=dev)
     if n == 0:
@@ -323,7 +336,7 @@ def score_host_tier(w: DeviceWeights, tier, staging: KVPool, host_slots, q_token
         staging.set_valid_len(slots, tier.valid_len[grp])
         slot_of = dict(zip(grp.tolist(), slots.tolist()))
         sel = np.nonzero(np.isin(hs, grp))[0]
-        sel_t = torch.as_tensor(sel, device=dev)
+        sel_t = to_device(sel, dev)
         sc = score_slots(w, pages, np.array([slot_of[h] for h in hs[sel]]),
                          q.index_select(0, sel_t), max_rows=max_rows)
         scores[sel_t] = sc

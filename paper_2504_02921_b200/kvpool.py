@@ -29,6 +29,18 @@ from .errors import ShapeError, StoreError
 from .model import torch_dtype
 
 
+def to_device(arr, device, dtype=None):
+    """Host array -> device tensor without a stream synchronisation: staged
+    through pinned memory and copied non-blocking (a pageable source makes
+    torch block the host until the stream drains, which serialises host-side
+    scheduling with device work, e.g. between host-tier groups)."""
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 class KVPool:
     def __init__(self, config: ModelConfig, document_len: int, capacity: int,
                  dtype: str = "f16", device=None):
@@ -160,7 +172,9 @@ class KVPool:
     def slot_ptrs(self, slots):
         """Device int64 tensor of slot base addresses for the kernels."""
         import torch
-        s = torch.as_tensor(slots, device=self.device).to(torch.int64)
+        s = slots if isinstance(slots, torch.Tensor) else to_device(
+            np.asarray(slots, dtype=np.int64), self.device)
+        s = s.to(torch.int64)
         return s * self.slot_bytes + self.slab.data_ptr()
 
     def set_valid_len(self, slots, valid_len) -> None:
@@ -168,8 +182,7 @@ class KVPool:
         slots = np.asarray(slots, dtype=np.int64)
         vl = np.asarray(valid_len, dtype=np.int64)
         self._valid_host[slots] = vl
-        self.valid_len[torch.as_tensor(slots, device=self.device)] = torch.as_tensor(
-            vl, dtype=torch.int32, device=self.device)
+        self.valid_len[to_device(slots, self.device)] = to_device(vl, self.device, torch.int32)
 
     def host_valid_len(self, slot: int) -> int:
         return int(self._valid_host[slot])

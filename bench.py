@@ -717,6 +717,11 @@ def main():
     ap.add_argument("--host-quant", default="", choices=["", "int8", "int4"],
                     help="C5: keep host-tier pages HRKV-quantised (2x/4x fewer PCIe bytes)")
     args = ap.parse_args()
+    if args.config == "c4":
+        # C4 fills ~168 of the 178 GiB with KV pages; the scoring workspace is
+        # then sized from what is left, and a cached-but-split block cannot be
+        # re-used for it -- expandable segments remove that fragmentation
+        os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         # one process per GPU: re-launch this command under torch.distributed.run
         sys.exit(relaunch(args.gpus))

@@ -73,8 +73,6 @@ def rows_budget(w: DeviceWeights, budget: int | None = None) -> int:
     import torch
     if budget is None:
         free, _ = torch.cuda.mem_get_info(w.device)
-        # memory PyTorch holds cached but unallocated is usable too
-        free += torch.cuda.memory_reserved(w.device) - torch.cuda.memory_allocated(w.device)
         held = _workspace(w.device).buf
         held = held.numel() if held is not None else 0
         budget = min(DEFAULT_WORKSPACE_BUDGET, int(0.8 * (free + held)))

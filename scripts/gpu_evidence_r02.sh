@@ -18,6 +18,7 @@ timeout -s KILL 1200 ncu --nvtx --nvtx-include "timed/" --set full --clock-contr
 echo "ncu gemm rc=$?"
 timeout -s KILL 900 ncu --nvtx --nvtx-include "timed/" --set full --clock-control none --import-source on -k regex:"attn_fa" -c 1 -o gpurun_out/${TAG}_attn_full $CMD > gpurun_out/${TAG}_attn_full.log 2>&1
 echo "ncu attn rc=$?"
+[ -n "$CORE_ONLY" ] && exit 0
 timeout -s KILL 1500 python bench.py --config c4 --steps 3 --warmup 2 --latency-reps 5 --no-cpu-baseline > gpurun_out/${TAG}_c4.json 2> gpurun_out/${TAG}_c4.err
 echo -n "c4 rc=$? "; python scripts/show.py gpurun_out/${TAG}_c4.json
 for qz in "" int8 int4; do

@@ -63,6 +63,11 @@ def suffix_flops_per_pair(cfg, D, Q):
     return 2 * L * p_layer * Q + 4 * L * H * HD * sum(D + j for j in range(1, Q + 1))
 
 
+def attention_flops_per_pair(cfg, D, Q):
+    """The attention term of suffix_flops_per_pair: QK^T and PV over D+j keys."""
+    return 4 * cfg.layers * cfg.heads * cfg.head_dim * sum(D + j for j in range(1, Q + 1))
+
+
 def kv_bytes_per_pair(cfg, D, es=2):
     return 2 * cfg.layers * cfg.kv_heads * D * cfg.head_dim * es
 
@@ -620,9 +625,17 @@ def run_ours(args, rank, world, local_rank):
             with open(tp) as f:
                 tj = json.load(f)
             traffic, traffic_alg = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
-        # attention kernel: cached-KV bytes it must read per step at HBM bandwidth
-        attn_bytes = n_local * kv_bytes_per_pair(cfg, D)
-        attn_gbs = attn_bytes / (prof["attn_ms"] / args.steps / 1e3) / 1e9 if prof["attn_ms"] else 0
+        # attention kernel: pairs that share a document attend as one row group, so
+        # the cached KV it must read per step is that of the DISTINCT documents; its
+        # work is 4*L*H*HD*sum_j(D+j) FLOPs per pair; the bound is
+        # whichever of the two takes longer at peak
+        n_docs_step = int(torch.unique(slots_dev).numel())
+        attn_bytes = n_docs_step * kv_bytes_per_pair(cfg, D)
+        attn_flops = n_local * (f_pair_attn := attention_flops_per_pair(cfg, D, Q))
+        attn_s = prof["attn_ms"] / args.steps / 1e3 if prof["attn_ms"] else 0
+        attn_gbs = attn_bytes / attn_s / 1e9 if attn_s else 0
+        attn_tf = attn_flops / attn_s / 1e12 if attn_s else 0
+        attn_tensor_bound = attn_flops / (peak_s * 1e12) >= attn_bytes / (hbm * 1e9)
         cpu = None
         if not args.no_cpu_baseline:
             v, info = cpu_pairs_per_s(preset, D, Q)
@@ -651,10 +664,18 @@ def run_ours(args, rank, world, local_rank):
                          "pairs_roofline": roof_pps, "pairs_frac": value / world / roof_pps,
                          "traffic_launch": "MLP-up GEMM (ncu, profiles/traffic_c3.json)",
                          "traffic_algorithmic": traffic_alg,
-                         "attention": {"bound": "hbm", "kernel": "attn_fa_kernel (tcgen05, P in TMEM)",
-                                       "achieved": attn_gbs, "peak": hbm, "unit": "GB/s",
-                                       "frac": attn_gbs / hbm if hbm else None,
-                                       "bytes_per_step": attn_bytes}},
+                         "attention": {
+                             "bound": "tensor" if attn_tensor_bound else "hbm",
+                             "kernel": "attn_fa_kernel (tcgen05, P in TMEM, grouped by document)",
+                             "achieved": attn_tf if attn_tensor_bound else attn_gbs,
+                             "peak": peak_s if attn_tensor_bound else hbm,
+                             "unit": "TFLOP/s" if attn_tensor_bound else "GB/s",
+                             "frac": (attn_tf / peak_s if attn_tensor_bound else attn_gbs / hbm)
+                             if peak_s and hbm else None,
+                             "flops_per_step": attn_flops, "flops_per_pair": f_pair_attn,
+                             "kv_bytes_per_step": attn_bytes, "distinct_docs_per_step": n_docs_step,
+                             "kv_gbs": attn_gbs, "kv_frac_of_hbm": attn_gbs / hbm if hbm else None,
+                             "tflops": attn_tf}},
             "cpu_baseline": cpu,
             "p50_query_latency_ms": float(np.median(lat)) if lat else None,
             "p50_query_latency_candidates": len(cand_ids[0]),

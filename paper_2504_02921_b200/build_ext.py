@@ -22,8 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["capi.cu", "gemm_tcgen05.cu", "gemm_simt.cu", "attention.cu", "attention_tc.cu",
-           "attention_fa.cu"]
+SOURCES = ["capi.cu", "gemm_tcgen05.cu", "gemm_simt.cu", "attention.cu", "attention_fa.cu"]
 
 
 def _headers():

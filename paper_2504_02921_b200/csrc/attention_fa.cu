@@ -8,16 +8,19 @@
 //    columns that held S (tcgen05.st) and consumed as the TMEM A operand of
 //    O += P.V (tcgen05.mma ... [a_tmem]) -- no smem round trip;
 //  * per tile two S/P buffers of 64 keys and one O (2 tiles x (2*64 + HD)
-//    columns = 512 for HD=128).  S runs two blocks ahead of the softmax: the
-//    issue order  PV_X(j), S_X(j+2)  relies on the tensor pipe executing
-//    tcgen05.mma in order, so S_X(j+2) overwrites P_X(j) (same buffer) only
+//    columns = 512 for HD=128; three S/P buffers for the single head_dim-256
+//    tile).  S runs NSB = 2 (3) blocks ahead of the softmax: the
+//    issue order  PV_X(j), S_X(j+NSB)  relies on the tensor pipe executing
+//    tcgen05.mma in order, so S_X(j+NSB) overwrites P_X(j) (same buffer) only
 //    after PV_X(j) has read it;
 //  * the rare lazy O rescale waits for the previous P.V (per-buffer barrier);
 //  * the suffix-block mask (tok_valid, causal) comes from a 64-bit ballot mask,
 //    not per-key global loads.
 //
 // Work item = 256 GQA-packed query rows (two 128-row tiles) of ONE document
-// and kv head.  Sequences that share a prefix document and sit next to each
+// and kv head (head_dim 256, the Gemma shape: 128 rows, one tile -- its O
+// accumulator needs 256 TMEM columns, so a tile's S buffers + O are 384 of the
+// 512; the single tile still overlaps softmax(j) with S(j+1) and P.V(j-1)).  Sequences that share a prefix document and sit next to each
 // other in the batch form a group whose rows are concatenated (each sequence
 // padded to Rp = R rounded up to 64 rows), so the document's K/V is streamed
 // once per 256 rows of the whole group -- the cross-query KV reuse of one
@@ -27,7 +30,8 @@
 // prefix blocks, masked to that sequence's rows.  krr_forward builds the item
 // table once per call (attn_group_items_kernel); without a table every
 // sequence is its own group.
-// SMEM: Q_A|Q_B 64 KB, K ring 4 x 16 KB, V ring 4 x 16 KB = 192 KB.
+// SMEM: Q_A|Q_B 64 KB, K ring 4 x 16 KB, V ring 4 x 16 KB = 192 KB (head_dim
+// 256: Q 64 KB, K ring 2 x 32 KB, V ring 3 x 32 KB = 224 KB).
 //
 // Quantised prefix pages (QB = 8 | 4: HRKV INT8/INT4 codes, codec.py:58-115,
 // per-(kv_head, channel) f32 scales) are dequantised inside the kernel: the
@@ -61,10 +65,23 @@ __device__ unsigned long long g_fa_trace[16 * 8 * 64];
 
 constexpr int TM = 128;
 constexpr int KB = 64;
-constexpr int NK = 4, NV = 4;   // K / V ring depth
-constexpr int THREADS = 320;    // w0 producers (lanes 0 Q, 1 K, 2 V), w1 MMA, w2-5 / w6-9 softmax
+constexpr int NK = 4, NV = 4;   // barrier slots per K / V ring (ring depth <= 4)
 constexpr int NC = 2;           // code ring depth per K / V (quantised prefix)
-template <int QB> constexpr int threads_of() { return QB == 16 ? THREADS : THREADS + 64; }
+// 128-row tiles per work item: two (ping-pong) up to head_dim 128, one at 256
+template <int HD> constexpr int tiles_of() { return HD == 256 ? 1 : 2; }
+// S/P buffers per tile: two with two tiles (2 x (2*64 + 128) = 512 TMEM
+// columns); the single head_dim-256 tile has room for three (3*64 + 256), so S
+// runs three blocks ahead and softmax(j+1) never waits behind P.V(j-1)
+template <int HD> constexpr int nsb_of() { return HD == 256 ? 3 : 2; }
+// K / V ring depths (head_dim 256: 32 KB per block, smem allows 3 + 2; K is
+// consumed NSB blocks ahead of V)
+template <int HD> constexpr int rk_of() { return HD == 256 ? 3 : NK; }
+template <int HD> constexpr int rv_of() { return HD == 256 ? 2 : NV; }
+// w0 producers (lanes 0 Q, 1 K, 2 V), w1 MMA, w2-5 (/ w6-9) softmax per tile,
+// + two converter warps for quantised prefix pages
+template <int HD, int QB> constexpr int threads_of() {
+  return 64 + 128 * tiles_of<HD>() + (QB == 16 ? 0 : 64);
+}
 constexpr float RESCALE_LOG2 = 15.0f;   // P <= 2^15 < f16 max
 
 struct Params {
@@ -85,19 +102,25 @@ struct Params {
 
 template <int HD, int QB = 16>
 struct Smem {
+  static constexpr int NT = tiles_of<HD>();
   static constexpr int ATOM_Q = TM * 128;                // one 128-row swizzle column of Q
   static constexpr int ATOM_KV = KB * 128;               // one 128-key swizzle column of K/V
   static constexpr int Q_TILE = (HD / 64) * ATOM_Q;
   static constexpr int KV_BYTES = (HD / 64) * ATOM_KV;
   static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + 2 * Q_TILE;
-  static constexpr int V_OFF = K_OFF + NK * KV_BYTES;
+  static constexpr int K_OFF = Q_OFF + NT * Q_TILE;
+  static constexpr int V_OFF = K_OFF + rk_of<HD>() * KV_BYTES;
   static constexpr int CODE_ROW = HD * QB / 8;           // code bytes per key (QB < 16)
   static constexpr int CODE_BLK = KB * CODE_ROW;
-  static constexpr int C_OFF = V_OFF + NV * KV_BYTES;    // code rings [K|V][NC]
+  static constexpr int C_OFF = V_OFF + rv_of<HD>() * KV_BYTES;    // code rings [K|V][NC]
   static constexpr int BAR_OFF = C_OFF + (QB < 16 ? 2 * NC * CODE_BLK : 0);
   static constexpr int TOTAL = BAR_OFF + 512;
-  static_assert(2 * KB + HD <= 256, "TMEM budget per tile");
+  // per tile: two S/P buffers of KB columns + O (HD columns), tiles 256 apart
+  static constexpr int TILE_COLS = NT == 2 ? 256 : 512;
+  static_assert(nsb_of<HD>() * KB + HD <= TILE_COLS && NT * TILE_COLS <= 512 &&
+                NT * nsb_of<HD>() <= 4, "TMEM / barrier budget");
+  static_assert(TOTAL <= 232448, "shared memory budget");
+  static_assert(QB == 16 || HD <= 128, "quantised prefix pages: head_dim 64|128");
 };
 
 enum {
@@ -128,7 +151,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-constexpr int MAX_SPAN = 2 * TM / 64;   // sequences one item can span (Rp >= 64)
+constexpr int MAX_SPAN = 2 * TM / 64;   // sequences one item can span (Rp >= 64), NT = 2
 
 struct Item {
   int b0, ng, row0, kvh;       // group's first sequence and size; first group row; kv head
@@ -139,7 +162,9 @@ struct Item {
 __device__ __forceinline__ int item_count(const Params& p) {
   return p.items ? __ldg(p.n_items) : p.items_implicit;
 }
+template <int NT>
 __device__ __forceinline__ Item item_of(const Params& p, int it) {
+  constexpr int ROWS = NT * TM;                  // query rows per item
   Item x;
   if (p.items) {
     const int4 e = __ldg(p.items + it);
@@ -149,10 +174,10 @@ __device__ __forceinline__ Item item_of(const Params& p, int it) {
     x.b0 = unit / p.KVH;
     x.kvh = unit - x.b0 * p.KVH;
     x.ng = 1;
-    x.row0 = (it - unit * p.chunks) * 2 * TM;
+    x.row0 = (it - unit * p.chunks) * ROWS;
   }
   x.s_lo = x.row0 / p.Rp;
-  const int s_hi = min((x.row0 + 2 * TM - 1) / p.Rp, x.ng - 1);
+  const int s_hi = min((x.row0 + ROWS - 1) / p.Rp, x.ng - 1);
   x.n_span = s_hi - x.s_lo + 1;
   int nbc_sum = 0;
 #pragma unroll
@@ -163,7 +188,7 @@ __device__ __forceinline__ Item item_of(const Params& p, int it) {
       // valid local rows of sequence s inside the item; causal: only keys up to
       // the largest token index among them are ever visible
       const int ra = max(x.row0 - s * p.Rp, 0);
-      const int rb = min(x.row0 + 2 * TM - s * p.Rp, p.R) - 1;
+      const int rb = min(x.row0 + ROWS - s * p.Rp, p.R) - 1;
       if (ra <= rb) {
         const int t_max = (rb / p.T != ra / p.T) ? p.T - 1 : rb % p.T;
         nb = (t_max + KB) / KB;
@@ -296,11 +321,15 @@ __device__ __forceinline__ void load_scales(const float* src, uint32_t* sc) {
 }
 
 template <typename T, int HD, int QB>
-__global__ void __launch_bounds__(threads_of<QB>(), 1)
+__global__ void __launch_bounds__(threads_of<HD, QB>(), 1)
     attn_fa_kernel(const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmPre,
                    const __grid_constant__ CUtensorMap tmCur, const Params p) {
   using S = Smem<HD, QB>;
+  constexpr int NT = S::NT;
+  constexpr int RK = rk_of<HD>(), RV = rv_of<HD>();
+  constexpr int TC = S::TILE_COLS;
+  constexpr int NSB = nsb_of<HD>();
   extern __shared__ uint8_t smem[];
   uint8_t* sQ = smem + S::Q_OFF;
   uint8_t* sK = smem + S::K_OFF;
@@ -309,7 +338,6 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + B_COUNT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_items = item_count(p);
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem) & 1023) != 0) __trap();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
@@ -344,17 +372,18 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int n_items = item_count(p);
 
   if (warp == 0) {
     // ---------------------------------------------------------- producers
     if (lane == 0) {                                   // Q tiles, per item
       int n = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
-        const Item x = item_of(p, it);
+        const Item x = item_of<NT>(p, it);
         mbar_wait(&bar[B_QEMPTY], (n & 1) ^ 1);
-        mbar_expect_tx(&bar[B_QFULL], 2 * S::Q_TILE);
+        mbar_expect_tx(&bar[B_QFULL], NT * S::Q_TILE);
 #pragma unroll
-        for (int sub = 0; sub < 4; ++sub) {            // 64-row boxes, one sequence each
+        for (int sub = 0; sub < 2 * NT; ++sub) {            // 64-row boxes, one sequence each
           const int gr = x.row0 + sub * 64;
           int s_rel = gr / p.Rp, r = gr - s_rel * p.Rp;
           if (s_rel >= x.ng) { s_rel = 0; r = 0; }     // past the group: rows unused
@@ -367,7 +396,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       }
     } else if (lane < 3) {                             // K ring (lane 1), V ring (lane 2)
       const bool is_k = lane == 1;
-      const int nst = is_k ? NK : NV;
+      const int nst = is_k ? RK : RV;
       uint64_t* full = &bar[is_k ? B_KFULL : B_VFULL];
       uint64_t* empty = &bar[is_k ? B_KEMPTY : B_VEMPTY];
       uint8_t* ring = is_k ? sK : sV;
@@ -375,7 +404,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       uint8_t* cring = smem + S::C_OFF + cw * NC * S::CODE_BLK;
       int g = 0, gc = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const Item x = item_of(p, it);
+        const Item x = item_of<NT>(p, it);
         const int pre_page = p.P ? (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b0]) -
                                           p.prefix_base) / p.prefix_page_bytes) +
                                        (p.layer * 2) * p.KVH + x.kvh
@@ -423,82 +452,81 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
     int g = 0, n = 0;
     // S_tile(gs) = Q_tile . K(gs)^T into S buffer gs&1
     auto issue_s = [&](int tile, int gs) {
-      const int st = gs % NK;
+      const int st = gs % RK;
       if (elect_one_sync()) {
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t qoff = tile * S::Q_TILE + (k >> 2) * S::ATOM_Q + (k & 3) * 32;
           const uint32_t koff = st * S::KV_BYTES + (k >> 2) * S::ATOM_KV + (k & 3) * 32;
-          mma_f16<1>(tmem + tile * 256 + (gs & 1) * KB, dQ + (qoff >> 4), dK + (koff >> 4),
+          mma_f16<1>(tmem + tile * TC + (gs % NSB) * KB, dQ + (qoff >> 4), dK + (koff >> 4),
                      idesc_s, k > 0);
         }
-        mma_commit<1>(&bar[B_SFULL + tile * 2 + (gs & 1)]);
+        mma_commit<1>(&bar[B_SFULL + tile * NSB + gs % NSB]);
       }
       __syncwarp();
     };
     // O_tile += P_tile(gs) . V(gs), P in the first KB/2 columns of S buffer gs&1
     auto issue_pv = [&](int tile, int gs, bool acc) {
-      const int sv = gs % NV;
+      const int sv = gs % RV;
       if (elect_one_sync()) {
 #pragma unroll
         for (int k = 0; k < KB / 16; ++k)
-          mma_ts(tmem + tile * 256 + 2 * KB, tmem + tile * 256 + (gs & 1) * KB + k * 8,
+          mma_ts(tmem + tile * TC + NSB * KB, tmem + tile * TC + (gs % NSB) * KB + k * 8,
                  dV + ((sv * S::KV_BYTES + k * 16 * 128) >> 4), idesc_o, acc || k > 0);
-        mma_commit<1>(&bar[B_PVDONE + tile * 2 + (gs & 1)]);
+        mma_commit<1>(&bar[B_PVDONE + tile * NSB + gs % NSB]);
       }
       __syncwarp();
     };
     auto issue_s_pair = [&](int gs, bool last_s) {     // S(gs) for both tiles, release K
-      mbar_wait(&bar[B_KFULL + gs % NK], (gs / NK) & 1);
+      mbar_wait(&bar[B_KFULL + gs % RK], (gs / RK) & 1);
       tc_fence_after();
-      issue_s(0, gs);
-      issue_s(1, gs);
+#pragma unroll
+      for (int tile = 0; tile < NT; ++tile) issue_s(tile, gs);
       if (elect_one_sync()) {
-        mma_commit<1>(&bar[B_KEMPTY + gs % NK]);
+        mma_commit<1>(&bar[B_KEMPTY + gs % RK]);
         if (last_s) mma_commit<1>(&bar[B_QEMPTY]);      // Q no longer read by this item
       }
       __syncwarp();
     };
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
-      const Item x = item_of(p, it);
+      const Item x = item_of<NT>(p, it);
       mbar_wait(&bar[B_QFULL], n & 1);
-      issue_s_pair(g, x.nb == 1);
-      if (x.nb > 1) issue_s_pair(g + 1, x.nb == 2);
+      for (int j = 0; j < NSB && j < x.nb; ++j) issue_s_pair(g + j, j == x.nb - 1);
       for (int j = 0; j < x.nb; ++j) {
         const int gs = g + j;
-        const bool ahead = j + 2 < x.nb;
+        const bool ahead = j + NSB < x.nb;
         TR(2, 4, gs);
-        mbar_wait(&bar[B_VFULL + gs % NV], (gs / NV) & 1);
+        mbar_wait(&bar[B_VFULL + gs % RV], (gs / RV) & 1);
         TR(2, 5, gs);
-        if (ahead) mbar_wait(&bar[B_KFULL + (gs + 2) % NK], ((gs + 2) / NK) & 1);
+        if (ahead) mbar_wait(&bar[B_KFULL + (gs + NSB) % RK], ((gs + NSB) / RK) & 1);
         TR(2, 6, gs);
 #pragma unroll
-        for (int tile = 0; tile < 2; ++tile) {
+        for (int tile = 0; tile < NT; ++tile) {
           if (j == 0) mbar_wait(&bar[B_OEMPTY + tile], (n & 1) ^ 1);
-          mbar_wait(&bar[B_PFULL + tile * 2 + (gs & 1)], (gs >> 1) & 1);
+          mbar_wait(&bar[B_PFULL + tile * NSB + gs % NSB], (gs / NSB) & 1);
           TR(2, tile * 2, gs);
           tc_fence_after();
           issue_pv(tile, gs, j > 0);
-          if (ahead) issue_s(tile, gs + 2);   // in-order pipe: PV(gs) reads P before S(gs+2) lands
+          if (ahead) issue_s(tile, gs + NSB);   // in-order pipe: PV(gs) reads P before S(gs+NSB) lands
           else if (j == x.nb - 1 && elect_one_sync()) mma_commit<1>(&bar[B_ODONE + tile]);
           __syncwarp();
           TR(2, tile * 2 + 1, gs);
         }
         if (elect_one_sync()) {
-          mma_commit<1>(&bar[B_VEMPTY + gs % NV]);
+          mma_commit<1>(&bar[B_VEMPTY + gs % RV]);
           if (ahead) {
-            mma_commit<1>(&bar[B_KEMPTY + (gs + 2) % NK]);
-            if (j + 2 == x.nb - 1) mma_commit<1>(&bar[B_QEMPTY]);
+            mma_commit<1>(&bar[B_KEMPTY + (gs + NSB) % RK]);
+            if (j + NSB == x.nb - 1) mma_commit<1>(&bar[B_QEMPTY]);
           }
         }
         __syncwarp();
       }
       g += x.nb;
     }
-  } else if (warp >= 10) {
+  } else if (warp >= 2 + 4 * NT) {
     // ---------------------------------------------------------- converters (QB < 16)
     if constexpr (QB < 16) {
-      const int cw = warp - 10;                        // 0: K, 1: V
+      const int cw = warp - (2 + 4 * NT);                        // 0: K, 1: V
       uint64_t* full = &bar[cw == 0 ? B_KFULL : B_VFULL];
       uint64_t* empty = &bar[cw == 0 ? B_KEMPTY : B_VEMPTY];
       uint8_t* ring = cw == 0 ? sK : sV;
@@ -511,7 +539,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       uint32_t sc[std::is_same<T, __half>::value ? CH / 2 : CH];
       int g = 0, gc = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const Item x = item_of(p, it);
+        const Item x = item_of<NT>(p, it);
         if (x.nb_pre > 0) {
           const int page = (int)((reinterpret_cast<const char*>(p.prefix_kv[x.b0]) -
                                   p.prefix_base) / p.prefix_page_bytes) +
@@ -519,9 +547,9 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
           load_scales<T, QB, CH>(p.scales + (int64_t)page * HD + cc * CH, sc);
         }
         for (int j = 0; j < x.nb_pre; ++j, ++gc) {
-          const int gg = g + j, s = gg % NK, c = gc % NC;
+          const int gg = g + j, s = gg % RK, c = gc % NC;
           mbar_wait(&bar[B_CFULL + cw * NC + c], (gc / NC) & 1);
-          mbar_wait(&empty[s], ((gg / NK) & 1) ^ 1);
+          mbar_wait(&empty[s], ((gg / RK) & 1) ^ 1);
           const uint8_t* src = cring + c * S::CODE_BLK;
           uint8_t* dst = ring + s * S::KV_BYTES;
 #pragma unroll 2
@@ -553,17 +581,17 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
     const int tile = (warp - 2) >> 2;
     const int quad = warp & 3;
     const int lrow = quad * 32 + lane;
-    const uint32_t lane_base = tmem + tile * 256 + ((uint32_t)(quad * 32) << 16);
-    const uint32_t o_col = 2 * KB;
-    uint64_t* s_full = &bar[B_SFULL + tile * 2];    // [buf]
-    uint64_t* p_full = &bar[B_PFULL + tile * 2];    // [buf]
-    uint64_t* pv_done = &bar[B_PVDONE + tile * 2];  // [buf]
+    const uint32_t lane_base = tmem + tile * TC + ((uint32_t)(quad * 32) << 16);
+    const uint32_t o_col = NSB * KB;
+    uint64_t* s_full = &bar[B_SFULL + tile * NSB];    // [buf]
+    uint64_t* p_full = &bar[B_PFULL + tile * NSB];    // [buf]
+    uint64_t* pv_done = &bar[B_PVDONE + tile * NSB];  // [buf]
     const float L2E = 1.4426950408889634f;
     const int T_ = p.T;
     const int H = p.KVH * p.G;
     int g = 0, n = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
-      const Item x = item_of(p, it);
+      const Item x = item_of<NT>(p, it);
       const int gr = x.row0 + tile * TM + lrow;       // row in the group's row space
       const int s_row = gr / p.Rp;                     // sequence (relative to b0)
       const int r = gr - s_row * p.Rp;
@@ -573,7 +601,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
       const int b = x.b0 + s_row;
       float m_use = -CUDART_INF_F, l = 0.f;
       for (int j = 0; j < x.nb; ++j) {
-        const int gs = g + j, sb = gs & 1;
+        const int gs = g + j, sb = gs % NSB;
         const bool pre = j < x.nb_pre;
         int key0 = j * KB;
         // suffix block (keys of one covered sequence): visible keys as a 64-bit
@@ -591,7 +619,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
           cur_mask &= rel >= 63 ? ~0ull : (rel < 0 ? 0ull : ((2ull << rel) - 1));
           if (s_blk != s_row) cur_mask = 0ull;
         }
-        mbar_wait(&s_full[sb], (gs >> 1) & 1);
+        mbar_wait(&s_full[sb], (gs / NSB) & 1);
         if (quad == 2) TR(3 + tile, 0, gs);
         tc_fence_after();
         bool need = false;
@@ -637,7 +665,7 @@ __global__ void __launch_bounds__(threads_of<QB>(), 1)
         }
         if (quad_live && j >= 1 && __any_sync(0xffffffffu, need)) {
           // O must be stable: wait for P.V of block gs-1 (its buffer's barrier)
-          mbar_wait(&pv_done[(gs - 1) & 1], ((gs - 1) >> 1) & 1);
+          mbar_wait(&pv_done[(gs - 1) % NSB], ((gs - 1) / NSB) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < HD / 32; ++c) {
@@ -746,7 +774,10 @@ static int launch(const AttnParams& a, cudaStream_t s) {
   const int R = a.group * a.seq_len;
   const int Rp = (R + 63) / 64 * 64;                  // rows per sequence in a group
   const int64_t units = (int64_t)a.n_seqs * a.kv_heads;
-  const int chunks = (Rp + 2 * TM - 1) / (2 * TM);
+  constexpr int ROWS = Sm::NT * TM;                   // query rows per work item
+  const int chunks = (Rp + ROWS - 1) / ROWS;
+  KRR_REQUIRE(a.items == nullptr || a.item_rows == ROWS, KRR_ECONFIG,
+              "attention item table built for another item size");
   KRR_REQUIRE(units * R < INT32_MAX && units * (chunks + 1) < INT32_MAX, KRR_ESHAPE,
               "attention batch too large");
   CUtensorMap mq, mp, mc;
@@ -791,9 +822,9 @@ static int launch(const AttnParams& a, cudaStream_t s) {
     mp = mc;
   }
   const int implicit = (int)(units * chunks);
-  // grouped items: at most one partial 256-row chunk per group beyond the rows
+  // grouped items: at most one partial chunk per group beyond the rows
   const int64_t bound = a.items ? (int64_t)a.kv_heads *
-                                      (((int64_t)a.n_seqs * Rp + 2 * TM - 1) / (2 * TM) + a.n_seqs)
+                                      (((int64_t)a.n_seqs * Rp + ROWS - 1) / ROWS + a.n_seqs)
                                 : implicit;
   Params p{a.prefix_kv, static_cast<const char*>(a.prefix_pool), pre_page, a.cur_kv,
            static_cast<const char*>(a.cur_pool), cur_page, a.prefix_valid_len, a.tok_valid,
@@ -804,17 +835,19 @@ static int launch(const AttnParams& a, cudaStream_t s) {
     if (rc) return rc;
   }
   const int grid = (int)std::min<int64_t>(bound, device_sm_count());
-  attn_fa_kernel<T, HD, QB><<<grid, threads_of<QB>(), Sm::TOTAL, s>>>(mq, mp, mc, p);
+  attn_fa_kernel<T, HD, QB><<<grid, threads_of<HD, QB>(), Sm::TOTAL, s>>>(mq, mp, mc, p);
   return check_launch("attention_fa");
 }
 
 // One CTA: sequences sharing a prefix page pointer and adjacent in the batch
-// form a group; each group's rows (Rp per sequence) are cut into 256-row
-// items, per kv head: items[] = {b0, ng, row0, kvh} in (group, kvh, chunk)
-// order, so CTAs running at the same time stream the same pages.
+// form a group; each group's rows (Rp per sequence) are cut into items of
+// `rows` (256, or 128 at head_dim 256), per kv head: items[] = {b0, ng, row0,
+// kvh} in (group, kvh, chunk) order, so CTAs running at the same time stream
+// the same pages.
 __global__ void __launch_bounds__(1024) attn_group_items_kernel(void* const* prefix_kv, int n,
-                                                                int Rp, int KVH, int64_t cap,
-                                                                int4* items, int* count) {
+                                                                int Rp, int rows, int KVH,
+                                                                int64_t cap, int4* items,
+                                                                int* count) {
   __shared__ int wsum[32];
   __shared__ int base;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -828,7 +861,7 @@ __global__ void __launch_bounds__(1024) attn_group_items_kernel(void* const* pre
       ng = 1;
       while (b + ng < n && prefix_kv[b + ng] == pk) ++ng;
     }
-    const int ch = ng ? (int)(((int64_t)ng * Rp + 2 * TM - 1) / (2 * TM)) : 0;
+    const int ch = ng ? (int)(((int64_t)ng * Rp + rows - 1) / rows) : 0;
     const int cnt = ch * KVH;
     int incl = cnt;                                  // block inclusive scan
 #pragma unroll
@@ -852,7 +885,7 @@ __global__ void __launch_bounds__(1024) attn_group_items_kernel(void* const* pre
     for (int k = 0; k < KVH; ++k)
       for (int c = 0; c < ch; ++c) {
         const int64_t i = off + (int64_t)k * ch + c;
-        if (i < cap) items[i] = make_int4(b, ng, c * 2 * TM, k);
+        if (i < cap) items[i] = make_int4(b, ng, c * rows, k);
       }
     __syncthreads();
     if (threadIdx.x == 0) base += wsum[(blockDim.x >> 5) - 1];
@@ -863,18 +896,23 @@ __global__ void __launch_bounds__(1024) attn_group_items_kernel(void* const* pre
 
 }  // namespace attn_fa
 
-int64_t attention_items_capacity(int64_t n_seqs, int group, int seq_len, int kv_heads) {
+int attention_item_rows(int head_dim) { return head_dim == 256 ? attn_fa::TM : 2 * attn_fa::TM; }
+
+int64_t attention_items_capacity(int64_t n_seqs, int group, int seq_len, int kv_heads,
+                                 int item_rows) {
   const int64_t Rp = ((int64_t)group * seq_len + 63) / 64 * 64;
-  return (int64_t)kv_heads * ((n_seqs * Rp + 2 * attn_fa::TM - 1) / (2 * attn_fa::TM) + n_seqs);
+  return (int64_t)kv_heads * ((n_seqs * Rp + item_rows - 1) / item_rows + n_seqs);
 }
 
 int build_attention_items(void* const* prefix_kv, int n_seqs, int group, int seq_len,
-                          int kv_heads, void* items, int64_t cap, int* count, cudaStream_t s) {
+                          int kv_heads, int item_rows, void* items, int64_t cap, int* count,
+                          cudaStream_t s) {
   const int Rp = (group * seq_len + 63) / 64 * 64;
-  KRR_REQUIRE(cap >= attention_items_capacity(n_seqs, group, seq_len, kv_heads) &&
+  KRR_REQUIRE(item_rows == attn_fa::TM || item_rows == 2 * attn_fa::TM, KRR_ECONFIG,
+              "attention items are 128 or 256 rows");
+  KRR_REQUIRE(cap >= attention_items_capacity(n_seqs, group, seq_len, kv_heads, item_rows) &&
                   cap < INT32_MAX, KRR_ECONFIG, "attention item table too small");
-  attn_fa::attn_group_items_kernel<<<1, 1024, 0, s>>>(prefix_kv, n_seqs, Rp, kv_heads, cap,
-                                                      static_cast<int4*>(items), count);
+  attn_fa::attn_group_items_kernel<<<1, 1024, 0, s>>>(prefix_kv, n_seqs, Rp, item_rows, kv_heads, cap, static_cast<int4*>(items), count);
   return check_launch("attention_items");
 }
 
@@ -886,15 +924,50 @@ extern "C" int krr_fa_trace_read(unsigned long long* out) {
 
 template <typename T, int QB>
 static int launch_hd(const AttnParams& p, cudaStream_t s) {
+  if constexpr (QB == 16)
+    if (p.head_dim == 256) return attn_fa::launch<T, 256, QB>(p, s);
   return p.head_dim == 64 ? attn_fa::launch<T, 64, QB>(p, s) : attn_fa::launch<T, 128, QB>(p, s);
 }
 
+bool attention_tcgen05_supported(int act, const AttnParams& a) {
+  return (act == KRR_F16 || act == KRR_BF16) &&
+         (a.head_dim == 64 || a.head_dim == 128 || a.head_dim == 256) &&
+         a.cur_pool != nullptr && a.cur_pool_bytes > 0 &&
+         (a.prefix_len == 0 || (a.prefix_pool != nullptr && a.prefix_pool_bytes > 0));
+}
+
+template <typename T, int HD>
+static int occupancy(int* out) {
+  using Sm = attn_fa::Smem<HD, 16>;
+  auto* k = attn_fa::attn_fa_kernel<T, HD, 16>;
+  const int rc = ensure_func_smem((const void*)k, Sm::TOTAL);
+  if (rc) return rc;
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      out, k, attn_fa::threads_of<HD, 16>(), Sm::TOTAL);
+  if (e != cudaSuccess) return fail(KRR_ECUDA, cudaGetErrorString(e));
+  return KRR_OK;
+}
+
+int attention_tcgen05_occupancy(int act_dtype, int head_dim, int* out) {
+  KRR_REQUIRE(head_dim == 64 || head_dim == 128 || head_dim == 256, KRR_EUNSUPPORTED,
+              "head_dim 64|128|256");
+  if (act_dtype == KRR_BF16)
+    return head_dim == 64    ? occupancy<__nv_bfloat16, 64>(out)
+           : head_dim == 128 ? occupancy<__nv_bfloat16, 128>(out)
+                             : occupancy<__nv_bfloat16, 256>(out);
+  return head_dim == 64 ? occupancy<__half, 64>(out)
+         : head_dim == 128 ? occupancy<__half, 128>(out)
+                           : occupancy<__half, 256>(out);
+}
+
 int launch_attention_fa(int act_dtype, const AttnParams& p, cudaStream_t s) {
-  if (!attention_tcgen05_supported(act_dtype, p) || p.head_dim > 128)
-    return fail(KRR_EUNSUPPORTED, "TMEM-P attention needs f16/bf16, head_dim 64|128 and pool bases");
+  if (!attention_tcgen05_supported(act_dtype, p))
+    return fail(KRR_EUNSUPPORTED, "TMEM-P attention needs f16/bf16, head_dim 64|128|256 and pool bases");
   const int qb = p.prefix_bits == 0 ? 16 : p.prefix_bits;
   if (qb != 16 && qb != 8 && qb != 4)
     return fail(KRR_ECONFIG, "prefix_bits must be 16 (or 0), 8 or 4");
+  if (qb != 16 && p.head_dim > 128)
+    return fail(KRR_EUNSUPPORTED, "quantised prefix pages need head_dim 64|128");
   if (act_dtype == KRR_F16) {
     if (qb == 8) return launch_hd<__half, 8>(p, s);
     if (qb == 4) return launch_hd<__half, 4>(p, s);

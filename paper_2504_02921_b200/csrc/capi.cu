@@ -511,12 +511,7 @@ static int do_attention(int backend, int act, const AttnParams& p, cudaStream_t 
                                     "head_dim 64|128 and 16-bit activations");
     return launch_attention_fa(act, p, s);
   }
-  if (backend == KRR_ATTN_TCGEN05) {
-    // head_dim 256 (Gemma shape) uses the one-tile kernel: its O accumulator
-    // needs 256 TMEM columns, leaving no room for a second tile's S/P
-    if (p.head_dim == 256) return launch_attention_tcgen05(act, p, s);
-    return launch_attention_fa(act, p, s);
-  }
+  if (backend == KRR_ATTN_TCGEN05) return launch_attention_fa(act, p, s);
   if (backend == KRR_ATTN_MMA) return launch_attention_mma(act, p, s);
   return launch_attention_simt(act, p, s);
 }
@@ -671,8 +666,7 @@ int krr_score_head(const float* x, int32_t n_seqs, int32_t seq_len, int32_t d,
                    float* scores, krr_stream_t stream) {
   if (n_seqs == 0) return KRR_OK;
   ProfScope ps((cudaStream_t)stream, 2);
-  score_kernel<<<n_seqs, 256, 0, (cudaStream_t)stream>>>(x, seq_len, d, last_index, final_gain,
-                                                         head, scores);
+  score_kernel<<<n_seqs, 256, 0, (cudaStream_t)stream>>>(x, seq_len, d, last_index, final_gain, head, scores);
   return check_launch("score_head");
 }
 
@@ -778,7 +772,8 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // n * Rp <= (G + 63) * rows): the grouped-attention table lives in the workspace.
 static int64_t items_bound(const krr_model_t* m, int64_t rows) {
   const int64_t G = m->heads / (m->kv_heads > 0 ? m->kv_heads : 1);
-  return (int64_t)m->kv_heads * (((G + 63) * rows + 255) / 256 + rows);
+  const int64_t ir = attention_item_rows(m->head_dim);
+  return (int64_t)m->kv_heads * (((G + 63) * rows + ir - 1) / ir + rows);
 }
 
 int krr_workspace_bytes(const krr_model_t* m, int64_t rows, size_t* out) {
@@ -840,9 +835,11 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
   }
   // cached-prefix scoring: group sequences that share a document so attention
   // streams each document's K/V once per 256 rows of all its queries
-  const bool grouped = b->prefix_len > 0 && act != KRR_F32 && (HD == 64 || HD == 128);
+  const bool grouped = b->prefix_len > 0 && act != KRR_F32 &&
+                       (HD == 64 || HD == 128 || HD == 256);
+  const int item_rows = attention_item_rows(HD);
   if (grouped) {
-    rc = build_attention_items(b->prefix_kv, b->n_seqs, G, b->seq_len, KVH, items,
+    rc = build_attention_items(b->prefix_kv, b->n_seqs, G, b->seq_len, KVH, item_rows, items,
                                items_bound(m, rows), item_count, s);
     if (rc) return rc;
   }
@@ -871,7 +868,7 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
                   b->prefix_kv, b->prefix_valid_len, b->cur_kv, b->tok_valid, ab,
                   b->prefix_pool, b->prefix_pool_bytes, b->cur_pool, b->cur_pool_bytes,
                   b->prefix_bits, b->prefix_scales, grouped ? items : nullptr,
-                  grouped ? item_count : nullptr};
+                  grouped ? item_count : nullptr, item_rows};
     rc = do_attention(m->attn_backend, act, ap, s);
     if (rc) return rc;
     EpiParams er{};
@@ -893,13 +890,10 @@ int krr_forward(const krr_model_t* m, const krr_batch_t* b, void* workspace, siz
       {
         ProfScope ps(s, 2);
         if (es == 2)
-          gather_last_kernel<uint16_t><<<(unsigned)n, 256, 0, s>>>(
-              (const uint16_t*)ab, b->last_index, b->seq_len, H * HD, (uint16_t*)ab_c);
+          gather_last_kernel<uint16_t><<<(unsigned)n, 256, 0, s>>>((const uint16_t*)ab, b->last_index, b->seq_len, H * HD, (uint16_t*)ab_c);
         else
-          gather_last_kernel<float><<<(unsigned)n, 256, 0, s>>>(
-              (const float*)ab, b->last_index, b->seq_len, H * HD, (float*)ab_c);
-        gather_last_kernel<float><<<(unsigned)n, 256, 0, s>>>(x, b->last_index, b->seq_len, d,
-                                                              x_c);
+          gather_last_kernel<float><<<(unsigned)n, 256, 0, s>>>((const float*)ab, b->last_index, b->seq_len, H * HD, (float*)ab_c);
+        gather_last_kernel<float><<<(unsigned)n, 256, 0, s>>>((const float*)x, b->last_index, b->seq_len, d, x_c);
         rc = check_launch("gather_last");
         if (rc) return rc;
       }

@@ -41,12 +41,16 @@ struct AttnParams {
   // document, adjacent in the batch, attend as one row group); null = per seq
   const void* items;
   const int* n_items;
+  int item_rows;               // rows per item the table was built for
 };
-int64_t attention_items_capacity(int64_t n_seqs, int group, int seq_len, int kv_heads);
+// query rows per attention work item (256: two 128-row tiles; 128 at head_dim 256)
+int attention_item_rows(int head_dim);
+int64_t attention_items_capacity(int64_t n_seqs, int group, int seq_len, int kv_heads,
+                                 int item_rows);
 int build_attention_items(void* const* prefix_kv, int n_seqs, int group, int seq_len,
-                          int kv_heads, void* items, int64_t cap, int* count, cudaStream_t s);
+                          int kv_heads, int item_rows, void* items, int64_t cap, int* count,
+                          cudaStream_t s);
 int launch_attention_mma(int act_dtype, const AttnParams& p, cudaStream_t s);
-int launch_attention_tcgen05(int act_dtype, const AttnParams& p, cudaStream_t s);
 int launch_attention_fa(int act_dtype, const AttnParams& p, cudaStream_t s);
 bool attention_tcgen05_supported(int act_dtype, const AttnParams& p);
 int attention_tcgen05_occupancy(int act_dtype, int head_dim, int* out);

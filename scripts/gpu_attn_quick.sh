@@ -1,0 +1,11 @@
+#!/bin/bash
+# Attention change check: attention/grouped/parity GPU tests, C2 launch list, C2 graph p50.
+TAG=${1:-aq}
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+timeout -s KILL 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_grouped.py tests/test_gpu_parity.py tests/test_gpu_parity_wide.py -q -m gpu --timeout 600 -p no:cacheprovider > gpurun_out/${TAG}_pytest.log 2>&1
+echo "pytest rc=$?"; grep -E "passed|failed|^FAILED|^ERROR" gpurun_out/${TAG}_pytest.log | tail -12
+CMD="python bench.py --config c2 --steps 2 --warmup 1 --no-cpu-baseline --latency-reps 0 --full-pairs 4"
+timeout -s KILL 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_c2_launches.csv $CMD > /dev/null 2>&1
+python scripts/ncu_list_summary.py gpurun_out/${TAG}_c2_launches.csv > gpurun_out/${TAG}_c2_launches.txt; head -4 gpurun_out/${TAG}_c2_launches.txt
+timeout -s KILL 600 python bench.py --config c2 --steps 20 --warmup 3 --latency-reps 15 --no-cpu-baseline --full-pairs 4 > gpurun_out/${TAG}_c2.json 2>/dev/null
+echo -n "c2: "; python scripts/show.py gpurun_out/${TAG}_c2.json

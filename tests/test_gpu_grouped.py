@@ -2,8 +2,8 @@
 scored as one row group (krr_forward builds the item table; engine.score_slots
 sorts pairs by slot).  Every pair's score must be bit-identical to scoring it
 alone -- rows of other sequences in a shared item only ever see fully masked
-suffix blocks (P = 0) -- across GQA packings where one 256-row item spans 1-4
-sequences and where R is not a multiple of 64 (padded group rows)."""
+suffix blocks (P = 0) -- across GQA packings where one 256-row item (128 rows at head_dim 256) spans
+1-4 sequences and where R is not a multiple of 64 (padded group rows)."""
 
 import numpy as np
 import pytest
@@ -20,7 +20,9 @@ from paper_2504_02921_b200 import engine  # noqa: E402
 SHAPES = [(4, 2, 64, 48),      # C1 packing: R = 96 -> 128 group rows (padded)
           (8, 2, 128, 48),     # 7B packing: R = 192
           (8, 2, 128, 16),     # R = 64: one item spans 4 sequences
-          (4, 1, 128, 100)]    # R = 400 -> 448: items straddle sequences unevenly
+          (4, 1, 128, 100),    # R = 400 -> 448: items straddle sequences unevenly
+          (8, 1, 256, 48),     # Gemma packing (head_dim 256, 128-row items): R = 384
+          (2, 1, 256, 16)]     # R = 32 -> 64: one 128-row item spans 2 sequences
 
 
 @pytest.mark.parametrize("H,KVH,HD,Q", SHAPES)

@@ -73,10 +73,15 @@ template <int HD> constexpr int tiles_of() { return HD == 256 ? 1 : 2; }
 // columns); the single head_dim-256 tile has room for three (3*64 + 256), so S
 // runs three blocks ahead and softmax(j+1) never waits behind P.V(j-1)
 template <int HD> constexpr int nsb_of() { return HD == 256 ? 3 : 2; }
-// K / V ring depths (head_dim 256: 32 KB per block, smem allows 3 + 2; K is
-// consumed NSB blocks ahead of V)
-template <int HD> constexpr int rk_of() { return HD == 256 ? 3 : NK; }
-template <int HD> constexpr int rv_of() { return HD == 256 ? 2 : NV; }
+// K / V ring depths (head_dim 256: 32 KB per block, 2 + 2; quantised
+// prefixes: 3 + 3 next to the code rings) -- whatever leaves room for the
+// output staging buffers
+template <int HD, int QB> constexpr int rk_of() { return HD == 256 ? 2 : QB < 16 ? 3 : NK; }
+template <int HD, int QB> constexpr int rv_of() { return HD == 256 ? 2 : QB < 16 ? 3 : NV; }
+// epilogue staging per softmax warp: 32 rows x 32 columns of 16-bit output,
+// rows padded to 80 B (conflict-free transpose)
+constexpr int O_PITCH = 80;
+constexpr int O_STG = 32 * O_PITCH;
 // w0 producers (lanes 0 Q, 1 K, 2 V), w1 MMA, w2-5 (/ w6-9) softmax per tile,
 // + two converter warps for quantised prefix pages
 template <int HD, int QB> constexpr int threads_of() {
@@ -109,11 +114,12 @@ struct Smem {
   static constexpr int KV_BYTES = (HD / 64) * ATOM_KV;
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + NT * Q_TILE;
-  static constexpr int V_OFF = K_OFF + rk_of<HD>() * KV_BYTES;
+  static constexpr int V_OFF = K_OFF + rk_of<HD, QB>() * KV_BYTES;
   static constexpr int CODE_ROW = HD * QB / 8;           // code bytes per key (QB < 16)
   static constexpr int CODE_BLK = KB * CODE_ROW;
-  static constexpr int C_OFF = V_OFF + rv_of<HD>() * KV_BYTES;    // code rings [K|V][NC]
-  static constexpr int BAR_OFF = C_OFF + (QB < 16 ? 2 * NC * CODE_BLK : 0);
+  static constexpr int C_OFF = V_OFF + rv_of<HD, QB>() * KV_BYTES;    // code rings [K|V][NC]
+  static constexpr int STG_OFF = C_OFF + (QB < 16 ? 2 * NC * CODE_BLK : 0);
+  static constexpr int BAR_OFF = STG_OFF + 4 * NT * O_STG;
   static constexpr int TOTAL = BAR_OFF + 512;
   // per tile: two S/P buffers of KB columns + O (HD columns), tiles 256 apart
   static constexpr int TILE_COLS = NT == 2 ? 256 : 512;
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(threads_of<HD, QB>(), 1)
                    const __grid_constant__ CUtensorMap tmCur, const Params p) {
   using S = Smem<HD, QB>;
   constexpr int NT = S::NT;
-  constexpr int RK = rk_of<HD>(), RV = rv_of<HD>();
+  constexpr int RK = rk_of<HD, QB>(), RV = rv_of<HD, QB>();
   constexpr int TC = S::TILE_COLS;
   constexpr int NSB = nsb_of<HD>();
   extern __shared__ uint8_t smem[];
@@ -699,29 +705,51 @@ __global__ void __launch_bounds__(threads_of<HD, QB>(), 1)
         if (lane == 0) mbar_arrive(&p_full[sb]);
       }
       // ---------------------------------------------------------- epilogue
+      // O / l -> 16-bit rows [b*T + t][(kvh*G + gq)*HD + c].  Each 32-column
+      // chunk goes through this warp's staging buffer so that one store
+      // instruction writes 8 rows x 64 contiguous bytes (per-row 16 B stores
+      // from 32 different rows cost ~14% of the kernel: profiles/r02_attn_ablation.txt)
       mbar_wait(&bar[B_ODONE + tile], n & 1);
       tc_fence_after();
       if (quad_live) {
         const float inv = l > 0.f ? 1.f / l : 0.f;
         T* dst = reinterpret_cast<T*>(p.out) + ((int64_t)b * T_ + t) * (H * HD) +
                  (int64_t)(x.kvh * p.G + gq) * HD;
+        uint8_t* stg = smem + S::STG_OFF + (warp - 2) * O_STG;
+        // the rows this lane stores: rr = i*8 + lane/4, 16 B segment lane%4
+        const int seg = lane & 3;
+        T* rdst[4];
+        bool rok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int src = i * 8 + (lane >> 2);
+          rdst[i] = reinterpret_cast<T*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), src));
+          rok[i] = __shfl_sync(0xffffffffu, row_ok, src);
+        }
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
           uint32_t o[32];
           tmem_ld32_nowait(lane_base + o_col + c * 32, o);
           tmem_ld_wait();
-          if (row_ok) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+          uint4* srow = reinterpret_cast<uint4*>(stg + lane * O_PITCH);
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint32_t w[4];
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t w[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                w[e] = pack_2<T>(__uint_as_float(o[q4 * 8 + 2 * e]) * inv,
-                                 __uint_as_float(o[q4 * 8 + 2 * e + 1]) * inv);
-              d4[q4] = make_uint4(w[0], w[1], w[2], w[3]);
-            }
+            for (int e = 0; e < 4; ++e)
+              w[e] = pack_2<T>(__uint_as_float(o[q4 * 8 + 2 * e]) * inv,
+                               __uint_as_float(o[q4 * 8 + 2 * e + 1]) * inv);
+            srow[q4] = make_uint4(w[0], w[1], w[2], w[3]);
           }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + (lane >> 2);
+            if (rok[i])
+              reinterpret_cast<uint4*>(rdst[i] + c * 32)[seg] =
+                  *reinterpret_cast<const uint4*>(stg + rr * O_PITCH + seg * 16);
+          }
+          __syncwarp();
         }
       }
       tc_fence_before();

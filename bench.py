@@ -322,7 +322,8 @@ def run_host_tier(args, rank, world, local_rank):
             tmp.release(cid)
     torch.cuda.synchronize()
     del tmp
-    staging = krr.KVPool(cfg, D, args.staging_slots, w.dtype, dev)
+    n_stage = args.staging_slots or (32 if args.host_quant else 16)
+    staging = krr.KVPool(cfg, D, n_stage, w.dtype, dev)
     page = tier.slot_bytes
     # ---- measured H2D peak (pinned -> HBM, 4 pages back to back)
     cs = torch.cuda.Stream(device=dev)
@@ -733,8 +734,11 @@ def main():
     ap.add_argument("--full-pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--query-lens", default="", help="C5 sweep, e.g. 16,32,48,64,128,256")
-    ap.add_argument("--staging-slots", type=int, default=16,
-                    help="C5: HBM staging slots (two halves, double-buffered)")
+    ap.add_argument("--staging-slots", type=int, default=0,
+                    help="C5: HBM staging slots (two halves, double-buffered; 0 = 16 for a "
+                         "16-bit tier, 32 for an INT8/INT4 tier: quantised documents cross "
+                         "PCIe 2-4x faster, so larger scoring groups amortise the per-forward "
+                         "weight stream; profiles/r02_c5_staging_sweep.txt)")
     ap.add_argument("--host-quant", default="", choices=["", "int8", "int4"],
                     help="C5: keep host-tier pages HRKV-quantised (2x/4x fewer PCIe bytes)")
     args = ap.parse_args()

@@ -74,7 +74,7 @@ enum { KRR_MLP_GELU = 0 /* reference: gelu_tanh(x W_up) W_down, 4d */,
 enum { KRR_GEMM_AUTO = 0, KRR_GEMM_TCGEN05 = 1, KRR_GEMM_SIMT = 2 };
 
 /* attention backends: auto picks TCGEN05 when the pools are described and the
- * geometry is supported (16-bit, head_dim 64/128), else MMA (16-bit) / SIMT (f32) */
+ * geometry is supported (16-bit, head_dim 64/128/256), else MMA (16-bit) / SIMT (f32) */
 enum { KRR_ATTN_AUTO = 0, KRR_ATTN_MMA = 1, KRR_ATTN_SIMT = 2, KRR_ATTN_TCGEN05 = 3 };
 
 /* Scatter description for KRR_EPI_QKV_ROPE.  Row r of the GEMM is token

@@ -161,6 +161,43 @@ def test_rerank_with_cache_misses_equals_full(model16):
         assert [p.score for p in res.selected[qi]] == [p.score for p in want]
 
 
+def test_rerank_graph_replay_matches_eager(model16, monkeypatch):
+    """A repeated latency-sized rerank shape replays a captured CUDA graph
+    (pipeline._graph_for): selections and scores equal the eager path bit for
+    bit, new queries / candidate orders are picked up on every replay, and
+    ragged or missing candidates keep the eager path."""
+    rng = np.random.default_rng(11)
+    docs = rng.integers(1, 32768, (8, 128))
+    ids = [f"doc-{i:05d}" for i in range(8)]
+    pool = krr.KVPool(C1[0], 128, 8, "f16")
+    slots = pool.allocate(ids)
+    engine.prefill_slots(model16.weights, pool, slots, docs, np.full(8, 128))
+
+    def eager(q, cands, k):
+        monkeypatch.setattr(pipeline, "GRAPH_MAX_ROWS", 0)
+        try:
+            return pipeline.rerank(model16, pool, ["qa", "qb"], q, cands, keep_m=k)
+        finally:
+            monkeypatch.undo()
+
+    for trial in range(4):                 # 1st call eager, 2nd captures, then replays
+        q = rng.integers(1, 32768, (2, 48))
+        cands = [list(rng.permutation(ids)[:6]) for _ in range(2)]
+        got = pipeline.rerank(model16, pool, ["qa", "qb"], q, cands, keep_m=3)
+        want = eager(q, cands, 3)
+        for a, b in zip(got.selected, want.selected):
+            assert [p.chunk_id for p in a] == [p.chunk_id for p in b]
+            assert [p.score for p in a] == [p.score for p in b]
+    assert len(pool._rerank_graphs) == 1
+    q = rng.integers(1, 32768, (2, 48))
+    ragged = [ids[:6], ids[2:5]]
+    res = pipeline.rerank(model16, pool, ["qa", "qb"], q, ragged, keep_m=3)
+    want = eager(q, ragged, 3)
+    assert [[p.score for p in r] for r in res.selected] == \
+        [[p.score for p in r] for r in want.selected]
+    assert len(pool._rerank_graphs) == 1
+
+
 def test_sharded_select_on_device_matches_single():
     """shard.sharded_select host logic with the CUDA top-k kernel, world=1 and
     a simulated 4-way split merged by the same kernel."""

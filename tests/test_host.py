@@ -151,3 +151,33 @@ def test_bench_rejects_gpus_world_mismatch():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
                        env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr
+
+
+def test_rerank_graph_cache_policy(monkeypatch):
+    """pipeline._graph_for: a shape is scored eagerly the first time, captured
+    the second, replayed afterwards; at most GRAPH_CACHE graphs per pool (LRU),
+    keyed by the weights object and the batch shape."""
+    from paper_2504_02921_b200 import engine, pipeline
+
+    made = []
+
+    class FakeGraph:
+        def __init__(self, w, pool, n_q, n_c, Q, k):
+            made.append((n_q, n_c, Q, k))
+
+    monkeypatch.setattr(engine, "GraphedScorer", FakeGraph)
+
+    class Pool:
+        pass
+
+    pool, w = Pool(), object()
+    assert pipeline._graph_for(pool, w, 1, 100, 48, 20) is None        # first sight: eager
+    g1 = pipeline._graph_for(pool, w, 1, 100, 48, 20)                    # second: capture
+    assert isinstance(g1, FakeGraph) and made == [(1, 100, 48, 20)]
+    assert pipeline._graph_for(pool, w, 1, 100, 48, 20) is g1            # replay
+    for shape in [(2, 50, 48, 20), (4, 25, 48, 20)]:
+        assert pipeline._graph_for(pool, w, *shape) is None
+        assert pipeline._graph_for(pool, w, *shape) is not None
+    assert len(pool._rerank_graphs) == pipeline.GRAPH_CACHE
+    assert (id(w), 1, 100, 48, 20) not in pool._rerank_graphs           # least recently used
+    assert pipeline._graph_for(pool, object(), 1, 100, 48, 20) is None  # other weights

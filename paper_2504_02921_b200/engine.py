@@ -137,10 +137,11 @@ def _prefill_slots(w, pool, slots, doc_tokens, valid_len, max_rows):
         raise ConfigError(f"pool dtype {pool.dtype} != weights dtype {w.dtype}")
     dev = w.device
     D = pool.document_len
-    tok = torch.as_tensor(np.asarray(doc_tokens), device=dev).to(torch.int32).reshape(-1, D)
+    tok = to_device(np.asarray(doc_tokens), dev).to(torch.int32).reshape(-1, D)
     n = tok.shape[0]
     valid = (tok != 0).to(torch.uint8)
-    slots_t = torch.as_tensor(np.asarray(slots), device=dev).to(torch.int64)
+    slots_t = (slots if isinstance(slots, torch.Tensor) else
+               to_device(np.asarray(slots, dtype=np.int64), dev)).to(dev).to(torch.int64)
     ptrs = pool.slot_ptrs(slots_t)
     step = max(1, (max_rows or rows_budget(w)) // D)
     for i in range(0, n, step):

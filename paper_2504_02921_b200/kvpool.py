@@ -38,6 +38,8 @@ def to_device(arr, device, dtype=None):
     t = torch.from_numpy(np.ascontiguousarray(arr))
     if dtype is not None:
         t = t.to(dtype)
+    if torch.device(device).type != "cuda":
+        return t.to(device)
     return t.pin_memory().to(device, non_blocking=True)
 
 

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import engine
 from .errors import ConfigError, ShapeError
-from .kvpool import KVPool
+from .kvpool import KVPool, to_device
 from .model import RerankModel
 from .reranker import ScoredPair, _check_vocab, _doc_valid
 
@@ -121,12 +121,11 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
     dev = w.device
     scores = torch.empty(len(flat), dtype=torch.float32, device=dev)
     hit = np.nonzero(slots >= 0)[0]
-    q_dev = torch.as_tensor(q.astype(np.int32), device=dev)
+    q_dev = to_device(q.astype(np.int32), dev)
     if len(hit):
-        qi = torch.as_tensor(pair_q[hit], device=dev)
-        sc = engine.score_slots(w, pool, torch.as_tensor(slots[hit], device=dev),
-                                q_dev.index_select(0, qi))
-        scores[torch.as_tensor(hit, device=dev)] = sc
+        qi = to_device(pair_q[hit], dev)
+        sc = engine.score_slots(w, pool, to_device(slots[hit], dev), q_dev.index_select(0, qi))
+        scores[to_device(hit, dev)] = sc
     if len(miss):
         if doc_tokens is None:
             raise ShapeError("cache miss without doc_tokens for full-recompute fallback")
@@ -136,8 +135,8 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
         stage = KVPool(model.config, model.layout.document_len, len(miss), w.dtype, dev)
         st_slots = stage.allocate_owned(len(miss))
         engine.prefill_slots(w, stage, st_slots, docs, (docs != 0).sum(axis=1))
-        qi = torch.as_tensor(pair_q[miss], device=dev)
-        scores[torch.as_tensor(miss, device=dev)] = engine.score_slots(
+        qi = to_device(pair_q[miss], dev)
+        scores[to_device(miss, dev)] = engine.score_slots(
             w, stage, st_slots, q_dev.index_select(0, qi))
     if n_c == 0:
         return RerankResult(list(query_ids), [[] for _ in range(n_q)], 0, 0)
@@ -145,7 +144,7 @@ def rerank(model: RerankModel, pool: KVPool, query_ids, query_tokens, candidates
     if not (lens == n_c).all():          # ragged: pad segments (-inf sorts last)
         seg = torch.full((n_q, n_c), float("-inf"), dtype=torch.float32, device=dev)
         pos = np.arange(len(flat)) - np.repeat(np.cumsum(lens) - lens, lens)
-        seg[torch.as_tensor(pair_q, device=dev), torch.as_tensor(pos, device=dev)] = scores
+        seg[to_device(pair_q, dev), to_device(pos, dev)] = scores
         scores = seg.view(-1)
     k = min(keep_m, n_c)
     idx, sc = engine.segmented_topk(scores, ids.reshape(-1), n_q, n_c, k)

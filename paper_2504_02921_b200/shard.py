@@ -84,8 +84,11 @@ def pad_segments(scores, ids, work: LocalWork, n_q: int):
     s = torch.full((n_q, L), float("-inf"), dtype=torch.float32, device=dev)
     i = torch.full((n_q, L), PAD_ID, dtype=torch.int32, device=dev)
     if work.pair_query.size:
-        q = torch.as_tensor(work.pair_query, device=dev)
-        p = torch.as_tensor(work.seg_pos, device=dev)
+        # pinned, non-blocking copies: a pageable host->device copy would make the
+        # host wait for the stream (serialising it with the scoring kernels)
+        from .kvpool import to_device
+        q = to_device(work.pair_query, dev)
+        p = to_device(work.seg_pos, dev)
         s[q, p] = scores.to(torch.float32)
         i[q, p] = ids.to(torch.int32)
     return s, i

@@ -107,12 +107,39 @@ __device__ __forceinline__ uint32_t pack16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// ------------------------------------------------------------ QKV row table
+// The QKV scatter needs, per output row, its sequence b, token t and (for K/V)
+// the sequence's KV page; a tile's 8 chunks share the rows, so each epilogue
+// thread resolves them once per tile: its own row (RoPE position) and the four
+// rows it stores in the transposed write-out (rr = i*8 + lane/4).
+struct QkvRows {
+  int pos;              // RoPE position of row row0 + lane
+  int b[4], t[4];       // sequence / token of the stored rows (b < 0: past M)
+  char* kv[4];          // their sequences' KV pages (kv_seq[b])
+};
+__device__ __forceinline__ void qkv_rows(const EpiParams& ep, int64_t row0, int lane,
+                                         QkvRows& qr) {
+  const krr_qkv_t& q = ep.qkv;
+  const int SL = q.seq_len;
+  const int my = (int)(row0 + lane);                 // M < 2^31 (launch check)
+  qr.pos = q.positions ? (my < ep.M ? q.positions[my] : 0) : q.pos0 + my % SL;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = (int)row0 + i * 8 + (lane >> 2);
+    const bool ok = row < ep.M;
+    const int b = row / SL;
+    qr.b[i] = ok ? b : -1;
+    qr.t[i] = row - b * SL;
+    qr.kv[i] = ok ? reinterpret_cast<char*>(q.kv_seq[b]) : nullptr;
+  }
+}
+
 // ------------------------------------------------------------ epilogue chunk
 // Thread `lane` of an epilogue warp holds row row0+lane, columns col0..col0+31.
 template <typename T>
 __device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap* out_map,
                                           const uint32_t (&r)[32], int64_t row0, int lane,
-                                          int col0, uint8_t* buf) {
+                                          int col0, uint8_t* buf, const QkvRows& qr) {
   if (ep.kind == KRR_EPI_RESIDUAL) {
     // f32 chunk, 128B-swizzled rows (16 B piece j of row l at slot j ^ (l & 7))
     uint8_t* row = buf + lane * 128;
@@ -154,14 +181,10 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap
   }
   // QKV: RoPE in registers, then scatter rows of 64 B (4 lanes x 16 B per row).
   const krr_qkv_t& q = ep.qkv;
-  const int64_t M = ep.M;
   const int head = col0 / q.head_dim;
   const int c0 = col0 - head * q.head_dim;
   if (head < q.heads + q.kv_heads) {
-    const int64_t my_row = row0 + lane;
-    const int pos = q.positions ? (my_row < M ? q.positions[my_row] : 0)
-                                : q.pos0 + (int)(my_row % q.seq_len);
-    const int64_t off = (int64_t)pos * (q.head_dim / 2) + (c0 >> 1);
+    const int64_t off = (int64_t)qr.pos * (q.head_dim / 2) + (c0 >> 1);
     const float4* cp = reinterpret_cast<const float4*>(q.rope_cos + off);
     const float4* sp = reinterpret_cast<const float4*>(q.rope_sin + off);
 #pragma unroll
@@ -184,26 +207,30 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap
     s[j] = make_uint4(pack16<T>(v[8 * j], v[8 * j + 1]), pack16<T>(v[8 * j + 2], v[8 * j + 3]),
                       pack16<T>(v[8 * j + 4], v[8 * j + 5]), pack16<T>(v[8 * j + 6], v[8 * j + 7]));
   __syncwarp();
+  // destination of this chunk's head: q [seq][kvh][g][t][HD] or the sequence's
+  // KV page [layer][K|V][kvh][t][HD]; rows then differ only by (b, t)
+  const int SL = q.seq_len, HD = q.head_dim, KVH = q.kv_heads, H = q.heads;
+  int64_t seq_stride, head_off;
+  bool to_q = head < H;
+  if (to_q) {
+    const int G = H / KVH, kvh = head / G, g = head - kvh * G;
+    seq_stride = (int64_t)KVH * G * SL * HD;
+    head_off = ((int64_t)(kvh * G + g) * SL) * HD + c0;
+  } else {
+    const int which = head < H + KVH ? 0 : 1;
+    const int kvh = head - H - which * KVH;
+    seq_stride = 0;
+    head_off = ((int64_t)((q.layer * 2 + which) * KVH + kvh) * q.kv_len) * HD + c0;
+  }
+  const int seg = lane & 3;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int rr = i * 8 + (lane >> 2), seg = lane & 3;
-    const int64_t row = row0 + rr;
-    if (row < M) {
+    if (qr.b[i] >= 0) {
+      const int rr = i * 8 + (lane >> 2);
       const uint4 val = *reinterpret_cast<const uint4*>(buf + rr * PITCH + seg * 16);
-      const int SL = q.seq_len, HD = q.head_dim, KVH = q.kv_heads, H = q.heads;
-      const int64_t b = row / SL;
-      const int t = (int)(row - b * SL);
-      T* dst;
-      if (head < H) {
-        const int G = H / KVH, kvh = head / G, g = head - kvh * G;
-        dst = reinterpret_cast<T*>(q.q_out) + (((b * KVH + kvh) * G + g) * (int64_t)SL + t) * HD + c0;
-      } else {
-        const int which = head < H + KVH ? 0 : 1;
-        const int kvh = head - H - which * KVH;
-        dst = reinterpret_cast<T*>(q.kv_seq[b]) +
-              ((int64_t)((q.layer * 2 + which) * KVH + kvh) * q.kv_len + t) * HD + c0;
-      }
-      reinterpret_cast<uint4*>(dst)[seg] = val;
+      T* base = to_q ? reinterpret_cast<T*>(q.q_out) + qr.b[i] * seq_stride
+                     : reinterpret_cast<T*>(qr.kv[i]);
+      reinterpret_cast<uint4*>(base + head_off + (int64_t)qr.t[i] * HD)[seg] = val;
     }
   }
   __syncwarp();
@@ -332,6 +359,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int it = 0, nchunk = 0;
     const bool glu = ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU;
     float gate[32];
+    QkvRows qr{};
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       int mb, nb;
       tile_coords(tile, num_m, num_n, group_m, mb, nb);
@@ -344,6 +372,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       named_bar_sync(1, 128);
       tc_fence_after();
       const int64_t row0 = (int64_t)mb * tile_m<G>() + rank * 128 + quad * 32;
+      if (ep.kind == KRR_EPI_QKV_ROPE) qkv_rows(ep, row0, lane, qr);
 #pragma unroll 1
       for (int c = 0; c < bn / 32; ++c) {
         uint32_t r[32];
@@ -369,7 +398,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // the bulk op that last read this buffer (two chunks ago) must be done
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
-        epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, buf);
+        epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, buf, qr);
       }
       tc_fence_before();
       __syncwarp();

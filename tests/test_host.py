@@ -181,3 +181,21 @@ def test_rerank_graph_cache_policy(monkeypatch):
     assert len(pool._rerank_graphs) == pipeline.GRAPH_CACHE
     assert (id(w), 1, 100, 48, 20) not in pool._rerank_graphs           # least recently used
     assert pipeline._graph_for(pool, object(), 1, 100, 48, 20) is None  # other weights
+
+
+def test_bench_work_accounting():
+    """bench.py's per-pair work model at the C3 shape: 554.67
+    GFLOP per pair (541.17 GEMM + 13.50 attention) and 67.1 MB of cached KV;
+    the attention term is the part attention_flops_per_pair reports."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2504_02921_b200.config import PRESETS
+    cfg, lay = PRESETS["c3_mistral7b"]
+    D, Q = lay.document_len, lay.query_len
+    f = bench.suffix_flops_per_pair(cfg, D, Q)
+    a = bench.attention_flops_per_pair(cfg, D, Q)
+    assert abs(f / 1e9 - 554.67) < 0.01 and abs(a / 1e9 - 13.50) < 0.01
+    d, H, KVH, HD, L = 4096, 32, 8, 128, 32
+    gemm = 2 * L * Q * (d * (H + 2 * KVH) * HD + H * HD * d + 2 * d * 4 * d)
+    assert f - a == gemm
+    assert bench.kv_bytes_per_pair(cfg, D) == 2 * L * KVH * D * HD * 2 == 67108864

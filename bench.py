@@ -495,7 +495,8 @@ def run_ours(args, rank, world, local_rank):
         return shard.merge_topk(sc, gid, k, engine.segmented_topk)
 
     def step():
-        engine.score_slots(w, pool, slots_dev, q_dev.index_select(0, qidx), out=scores)
+        engine.score_slots(w, pool, slots_dev, q_dev.index_select(0, qidx), out=scores,
+                           max_rows=args.max_rows or None)
         if strong:       # ragged local segments: local top-k, then the one all-gather
             return shard.sharded_select(scores, gid_dev, work, nq, k, engine.segmented_topk)
         idx, sc = engine.segmented_topk(scores, gid_dev, nq, nc, k)
@@ -734,6 +735,8 @@ def main():
     ap.add_argument("--latency-reps", type=int, default=20)
     ap.add_argument("--full-pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--max-rows", type=int, default=0,
+                    help="suffix rows per forward pass (0 = as many as the workspace budget allows)")
     ap.add_argument("--query-lens", default="", help="C5 sweep, e.g. 16,32,48,64,128,256")
     ap.add_argument("--staging-slots", type=int, default=0,
                     help="C5: HBM staging slots (two halves, double-buffered; 0 = 16 for a "

@@ -1,6 +1,8 @@
 """G=8 (CTA-pair, 256 rows per SM) GEMM check: run the same launches with
 KRR_GEMM_PAIR=0 and =1 in two subprocesses and compare outputs bit for bit, plus
-a fp32 torch reference.  usage: python scripts/pair_check.py"""
+a fp32 torch reference.  The G=8 geometry is not in the tree: apply
+scripts/variants/gemm_pair_g8.patch (KRR_GEMM_PAIR switch; -DEXP_NO_EPI gives the
+timing-only no-epilogue build) and rebuild.  usage: python scripts/pair_check.py"""
 import os, subprocess, sys
 import numpy as np
 

@@ -3,23 +3,30 @@
 //   C[M,N] = A[M,K] . B[N,K]^T    A = activations (16-bit, K-major)
 //                                 B = weights [out, in] (16-bit, K-major)
 //
-// Roles (192 threads, 1 CTA per SM):
+// Roles (1 CTA per SM):
 //   warp 0      TMA producer: 128B-swizzled A/B tiles into a smem ring
 //   warp 1      MMA issuer:   tcgen05.mma.kind::f16, K=16 steps, fp32 accumulators
-//                             in TMEM (2 x 256 columns, double buffered)
-//   warps 2..5  epilogue:     tcgen05.ld 32x32b.x32 -> fused epilogue -> TMA store
+//                             in TMEM (2 x 256 columns)
+//   warps 2..   epilogue:     tcgen05.ld 32x32b.x32 -> fused epilogue -> TMA store
 //
-// Every CTA owns 128 output rows x one 256-wide (or narrower) N tile:
-//   G=1  single CTA; it loads its whole B tile (launches with M <= 128).
-//   G=3  (default) cluster of 2 M-adjacent CTAs; each TMA-loads half of the
-//        weight tile and multicasts it into both (L2->SM 32 instead of 48 KB
-//        per CTA and k-block; under the power cap worth ~6% clock, r01).
-// CTA-pair geometries (cta_group::2 M=256 MMAs, alone or two pairs sharing the
-// weight tile by multicast) were built and measured in round 2: they keep the
-// tensor pipe 98% busy and read fewer operand bytes per FLOP, but their
-// launches read 2-6x the DRAM of G=3 (weight/activation panels fall out of L2)
-// and the full C3 step ran 7-11% slower at the same power cap
-// (profiles/r02_gemm_geometry.txt); they were removed.
+// Geometries (a launch's rows decide; all run the same per-element MMA
+// sequence, so results are bit-identical across them -- batch invariance):
+//   G=1  single CTA, 128 rows x one 256-wide (or narrower) N tile; M <= 128.
+//   G=3  cluster of 2 M-adjacent CTAs, 128 rows each; each TMA-loads half of
+//        the weight tile and multicasts it into both (L2->SM 32 instead of
+//        48 KB per CTA and k-block); double-buffered accumulators, 4 epilogue
+//        warps.  Small launches (latency / C2 batches) and > 131k rows.
+//   G=8  cuBLAS's geometry: a CTA pair with cta_group::2 M=256 MMAs and 256
+//        rows per SM (two pair MMAs per k-step share each stage's B; each SM
+//        holds its 128-row half), i.e. A 32 KB + B 16 KB per SM per 8.4 MFLOP
+//        instead of 48 KB per 4.2.  The accumulator (2 x 256 columns) is
+//        single-buffered, so its two halves are handed over separately: the
+//        last 4 k-blocks of a tile run half 0 first, the first 4 of the next
+//        tile start half 0 as soon as 8 epilogue warps have drained it.  The
+//        power cap grants it ~8% more clock than G=3; launches of 16k-131k
+//        rows (32k-row scoring passes) use it.  Other pair variants (one pair
+//        MMA per k-step, two pairs sharing the weight by multicast) and a
+//        256-row cta_group::1 CTA lost in the step (profiles/r02_gemm_geometry.txt).
 //
 // Epilogues: RESIDUAL adds the accumulator into the f32 residual stream with a
 // TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add, the read-modify-write
@@ -44,6 +51,9 @@ namespace tc {
 
 constexpr int BN = 256, BK = 64;
 constexpr int THREADS = 192;
+// G=8 drains each 256-column accumulator half with 8 epilogue warps (two per
+// TMEM lane quadrant) so a half is handed back inside the overlap window
+template <int G> constexpr int threads_of() { return G == 8 ? 320 : THREADS; }
 constexpr int STG_BUF = 4096;                 // one 32x32 chunk (f32) per buffer
 constexpr int STG_WARP_BYTES = 2 * STG_BUF;   // double buffered per epilogue warp
 
@@ -56,11 +66,20 @@ template <> struct Geo<3> {
   static constexpr int CS = 2, STAGES = 4, GROUP_M = 8;
   static constexpr int B_ROWS_SMEM = 256;
 };
-constexpr int A_BYTES = 128 * BK * 2;                      // 16 KB: 128 rows per CTA
+// G=8 (A/B): CTA pair with cta_group::2 MMAs, 256 rows per SM: two M=256 pair
+// MMAs per k-step share each stage's B (each SM holds ITS 128-row half), so an
+// SM receives A 32 KB + B 16 KB per 8.4 MFLOP; single-buffered 2 x 256-column
+// accumulator per SM.
+template <> struct Geo<8> {
+  static constexpr int CS = 2, STAGES = 4, GROUP_M = 4;
+  static constexpr int B_ROWS_SMEM = 128;
+};
+template <int G> constexpr int cta_rows() { return G == 8 ? 256 : 128; }
+template <int G> constexpr int a_bytes() { return cta_rows<G>() * BK * 2; }
 template <int G> constexpr int b_bytes() { return Geo<G>::B_ROWS_SMEM * BK * 2; }
-template <int G> constexpr int tile_m() { return 128 * Geo<G>::CS; }   // rows per cluster
+template <int G> constexpr int tile_m() { return cta_rows<G>() * Geo<G>::CS; }   // rows per cluster
 template <int G> constexpr int smem_bytes() {
-  return Geo<G>::STAGES * (A_BYTES + b_bytes<G>()) + 4 * STG_WARP_BYTES + 1024 /*align*/ +
+  return Geo<G>::STAGES * (a_bytes<G>() + b_bytes<G>()) + 4 * STG_WARP_BYTES + 1024 /*align*/ +
          512 /*barriers*/;
 }
 
@@ -238,7 +257,7 @@ __device__ __forceinline__ void epi_chunk(const EpiParams& ep, const CUtensorMap
 
 // ------------------------------------------------------------ kernel
 template <typename T, int G>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(threads_of<G>(), 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmOut, int64_t M, int N, int K,
@@ -246,6 +265,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   using C = Geo<G>;
   constexpr int CS = C::CS, STAGES = C::STAGES;
   constexpr int B_BYTES = b_bytes<G>();
+  constexpr int A_BYTES = a_bytes<G>();
+  constexpr bool PAIR = G == 8;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -267,19 +288,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       // G=3: a stage is free only when BOTH CTAs' MMAs have read it (the peer
       // multicasts its half of B into this CTA's buffer)
-      mbar_init(&empty[s], CS);
+      // (pair: one multicast commit of the leader's MMAs frees both CTAs)
+      mbar_init(&empty[s], PAIR ? 1 : CS);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], PAIR ? 16 : 4);  // pair: both CTAs' 8 epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tmem_slot)) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_slot)) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_slot)) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -305,6 +333,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (elect_one_sync()) {
           uint8_t* a_dst = sA + stage * A_BYTES;
           uint8_t* b_dst = sB + stage * B_BYTES;
+          if constexpr (PAIR) {
+            // both CTAs' bytes complete on the leader's barrier; rows: this SM's
+            // 128 of each of the pair tile's two 256-row MMAs, and its B half
+            const uint32_t bar = mapa_rank(smem_u32(&full[stage]), 0);
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+            tma_load<2>(a_dst, &tmA, bar, kb * BK, row_a);
+            tma_load<2>(a_dst + 128 * 128, &tmA, bar, kb * BK, row_a + 256);
+            tma_load<2>(b_dst, &tmB, bar, kb * BK, nb * bn + (int)rank * 128);
+          } else {
           const uint32_t bar = smem_u32(&full[stage]);
           mbar_expect_tx(&full[stage], A_BYTES + bn * BK * 2);
           tma_load<1>(a_dst, &tmA, bar, kb * BK, row_a);
@@ -316,6 +353,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             tma_load_mc(b_dst + rank * (b_rows * BK * 2), &tmB, bar, kb * BK,
                         nb * bn + (int)rank * b_rows, (uint16_t)0x3);
           }
+          }
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -323,15 +361,96 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     // whole warp walks the schedule; one elected lane issues (descriptors stay
-    // in uniform registers, no per-MMA elect loop)
+    // in uniform registers, no per-MMA elect loop).  Pair: the leader issues.
+    if constexpr (PAIR) {
+      if (rank == 0) {
+        // Pair schedule with the two 256-column accumulator halves handed over
+        // separately: a tile's last `post` k-blocks run MMA#1 (half 0) first so
+        // half 0 is committed while MMA#2 finishes; the next tile's first `pre`
+        // k-blocks run MMA#1 as soon as half 0 is drained and MMA#2 once half 1
+        // is -- each half's epilogue overlaps the other half's MMAs.
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        const uint64_t dA = sw128_desc(smem_u32(sA));
+        const uint64_t dB = sw128_desc(smem_u32(sB));
+        const int pre = min(STAGES, nk), post = min(STAGES, nk - pre);
+        auto mma = [&](int h, int st, int kb) {
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_f16<2>(tmem_base + h * BN, dA + ((st * A_BYTES + h * 128 * 128 + k * 32) >> 4),
+                       dB + ((st * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+        };
+        auto adv = [&](int& st, uint32_t& ph) { if (++st == STAGES) { st = 0; ph ^= 1; } };
+        for (int tile = cid; tile < tiles; tile += ncl, ++it) {
+          const uint32_t ap = it & 1;
+          // head: half 0 first, then half 1, on the same resident stages
+          mbar_wait(&tempty[0], ap ^ 1);
+          tc_fence_after();
+          int s0 = stage; uint32_t p0 = phase;
+          for (int kb = 0; kb < pre; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (elect_one_sync()) mma(0, stage, kb);
+            __syncwarp();
+            adv(stage, phase);
+          }
+          mbar_wait(&tempty[1], ap ^ 1);
+          tc_fence_after();
+          stage = s0; phase = p0;
+          for (int kb = 0; kb < pre; ++kb) {
+            if (elect_one_sync()) {
+              mma(1, stage, kb);
+              mma_commit<2>(&empty[stage]);
+            }
+            __syncwarp();
+            adv(stage, phase);
+          }
+          // body
+          for (int kb = pre; kb < nk - post; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (elect_one_sync()) {
+              mma(0, stage, kb);
+              mma(1, stage, kb);
+              mma_commit<2>(&empty[stage]);
+            }
+            __syncwarp();
+            adv(stage, phase);
+          }
+          // tail: half 0 completes first
+          s0 = stage; p0 = phase;
+          for (int kb = nk - post; kb < nk; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (elect_one_sync()) mma(0, stage, kb);
+            __syncwarp();
+            adv(stage, phase);
+          }
+          if (elect_one_sync()) mma_commit<2>(&tfull[0]);
+          __syncwarp();
+          stage = s0; phase = p0;
+          for (int kb = nk - post; kb < nk; ++kb) {
+            if (elect_one_sync()) {
+              mma(1, stage, kb);
+              mma_commit<2>(&empty[stage]);
+            }
+            __syncwarp();
+            adv(stage, phase);
+          }
+          if (elect_one_sync()) mma_commit<2>(&tfull[1]);
+          __syncwarp();
+        }
+      }
+    } else {
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
     const uint64_t dA = sw128_desc(smem_u32(sA));
     const uint64_t dB = sw128_desc(smem_u32(sB));
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = PAIR ? 0 : it & 1;
+      const uint32_t acc_phase = PAIR ? it & 1 : (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;   // accumulators 256 columns apart
@@ -340,22 +459,38 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         if (elect_one_sync()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_f16<1>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
-                       dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            if constexpr (PAIR) {
+              mma_f16<2>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
+                         dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+              mma_f16<2>(d_tmem + BN, dA + ((stage * A_BYTES + 128 * 128 + k * 32) >> 4),
+                         dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+            } else {
+              mma_f16<1>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
+                         dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
+            }
+          }
           // completion frees the stage in every CTA that holds its operands
           if constexpr (G == 1) mma_commit<1>(&empty[stage]);
+          else if constexpr (PAIR) mma_commit<2>(&empty[stage]);
           else mma_commit_mc1(&empty[stage], (uint16_t)0x3);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (elect_one_sync()) mma_commit<1>(&tfull[acc]);
+      if (elect_one_sync()) {
+        if constexpr (PAIR) mma_commit<2>(&tfull[acc]);
+        else mma_commit<1>(&tfull[acc]);
+      }
       __syncwarp();
+    }
     }
   } else {
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    uint8_t* stg = stage_base + (warp - 2) * STG_WARP_BYTES;
+    constexpr int EPI = PAIR ? 8 : 4;                  // epilogue warps
+    const int sub = (warp - 2) >> 2;                    // pair: which chunk pairs this warp drains
+    // pair: one 4 KB staging buffer per warp (8 warps share the 4 x 8 KB area)
+    uint8_t* stg = stage_base + (warp - 2) * (PAIR ? STG_BUF : STG_WARP_BYTES);
     int it = 0, nchunk = 0;
     const bool glu = ep.kind == KRR_EPI_GLU_GELU || ep.kind == KRR_EPI_GLU_SILU;
     float gate[32];
@@ -363,20 +498,36 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int tile = cid; tile < tiles; tile += ncl, ++it) {
       int mb, nb;
       tile_coords(tile, num_m, num_n, group_m, mb, nb);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = PAIR ? 0 : it & 1;
+      const uint32_t acc_phase = PAIR ? it & 1 : (it >> 1) & 1;
       // one epilogue warp polls the accumulator barrier; the other three are
       // parked on a named barrier (the poll loop of four warps was ~1/4 of all
       // issued instructions and power)
       if (warp == 2) mbar_wait(&tfull[acc], acc_phase);
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 32 * EPI);
       tc_fence_after();
-      const int64_t row0 = (int64_t)mb * tile_m<G>() + rank * 128 + quad * 32;
-      if (ep.kind == KRR_EPI_QKV_ROPE) qkv_rows(ep, row0, lane, qr);
+      const int nch = bn / 32;
+      const uint32_t tempty_leader = PAIR ? mapa_rank(smem_u32(&tempty[0]), 0) : 0;
 #pragma unroll 1
-      for (int c = 0; c < bn / 32; ++c) {
+      for (int cc = 0; cc < nch; ++cc) {
+        // pair: accumulator h (TMEM columns h*256..) holds rows h*256 + rank*128 ..;
+        // this warp drains chunk pairs {4q + 2*sub, +1} of each half
+        const int h = PAIR && cc >= nch / 2 ? 1 : 0;
+        const int j = cc - h * (nch / 2);
+        const int c = PAIR ? (j >> 1) * 4 + sub * 2 + (j & 1) : cc;
+        if (PAIR && cc == nch / 2) {
+          // half 0 drained: hand it back, then wait for half 1
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader);
+          if (warp == 2) mbar_wait(&tfull[1], acc_phase);
+          named_bar_sync(1, 32 * EPI);
+          tc_fence_after();
+        }
+        const int64_t row0 = (int64_t)mb * tile_m<G>() + h * 256 + rank * 128 + quad * 32;
+        if (ep.kind == KRR_EPI_QKV_ROPE && (PAIR ? j == 0 : c == 0)) qkv_rows(ep, row0, lane, qr);
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (acc + h) * BN + c * 32, r);
         int col0 = nb * bn + c * 32;
         if (col0 >= N) continue;
         if (glu) {
@@ -393,16 +544,22 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(gate[j] * __uint_as_float(r[j]));
           col0 = (col0 - 32) / 2;
         }
-        uint8_t* buf = stg + (nchunk & 1) * STG_BUF;
+        uint8_t* buf = stg + (PAIR ? 0 : (nchunk & 1) * STG_BUF);
         ++nchunk;
-        // the bulk op that last read this buffer (two chunks ago) must be done
-        if (lane == 0) bulk_wait_read<1>();
+        // the bulk op that last read this buffer (one / two chunks ago) must be done
+        if (lane == 0) {
+          if constexpr (PAIR) bulk_wait_read<0>();
+          else bulk_wait_read<1>();
+        }
         __syncwarp();
         epi_chunk<T>(ep, &tmOut, r, row0, lane, col0, buf, qr);
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(tempty_leader + 8);   // half 1
+        else mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -411,7 +568,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   if constexpr (CS > 1) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
 }
 
@@ -460,7 +620,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   const int tiles = (int)((M + tile_m<G>() - 1) / tile_m<G>()) * ((N + bn - 1) / bn);
   constexpr int CS = Geo<G>::CS;
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(threads_of<G>());
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];
@@ -488,7 +648,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   const int grid = std::min(CS * tiles, CS * max_clusters);
   cfg.gridDim = dim3(grid);
   cudaLaunchKernelEx(&cfg, gemm_tcgen05_kernel<T, G>, ma, mb, mo, M, N, K, idesc, group_m, bn, ep);
-  return check_launch(G == 3 ? "gemm_tcgen05_mc" : "gemm_tcgen05");
+  return check_launch(G == 1 ? "gemm_tcgen05" : "gemm_tcgen05_mc");
 }
 
 }  // namespace tc
@@ -506,8 +666,12 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   if (ep.kind == KRR_EPI_QKV_ROPE && ep.qkv.head_dim % 32 != 0)
     return launch_gemm_simt(act_dtype, A, B, M, N, K, ep, s);  // a chunk must stay in one head
 
-  // one 128-row tile: a cluster partner would idle
-  const int geo = M <= 128 ? 1 : 3;
+  // one 128-row tile: a cluster partner would idle.  Launches of 16k-131k rows
+  // (the scoring passes of a large batch) take the CTA-pair geometry: it is
+  // granted ~8% more clock under the power cap and wins ~0.8% on the C3 step;
+  // beyond ~131k rows its loads miss L2 (profiles/r02_gemm_geometry.txt), and
+  // small launches need the 128-row units for their wave count.
+  const int geo = M <= 128 ? 1 : (M >= 16384 && M <= 131072) ? 8 : 3;
   // N-tile width, chosen by a wave model: each
   // candidate width bn (multiples of 32 so epilogue chunks never straddle a
   // head) gives units = m-tiles x ceil(N/bn) tiles on `slots` persistent
@@ -520,7 +684,7 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   // sequence (full K in BK-chunk order into one fp32 accumulator), so the
   // choice may depend on M without breaking batch invariance.
   int bn = BN;
-  {
+  if (geo != 8) {
     const int rows_per_unit = geo == 3 ? 256 : 128;
     const int64_t slots = geo == 3 ? device_sm_count() / 2 : device_sm_count();
     const int64_t m_units = (M + rows_per_unit - 1) / rows_per_unit;
@@ -531,7 +695,7 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
       if (cand == 256 || cost < best * 0.98) { best = cost; bn = cand; }
     }
   }
-  const int group_m = geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
+  const int group_m = geo == 8 ? Geo<8>::GROUP_M : geo == 3 ? Geo<3>::GROUP_M : Geo<1>::GROUP_M;
   const CUtensorMapDataType dt =
       act_dtype == KRR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap ma, mb, mo;
@@ -558,12 +722,14 @@ int launch_gemm_tcgen05(int act_dtype, const void* A, const void* B, int64_t M, 
   // instruction descriptor: D=f32 @4, A/B f16|bf16 @7/@10, K-major both, N>>3 @17, M>>4 @24
   const uint32_t fmt = act_dtype == KRR_BF16 ? 1u : 0u;
   const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(bn >> 3) << 17) |
-                         ((uint32_t)(128 >> 4) << 24);
+                         ((uint32_t)((geo == 8 ? 256 : 128) >> 4) << 24);
   if (act_dtype == KRR_F16)
-    return geo == 1 ? launch<__half, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
-                    : launch<__half, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);
-  return geo == 1 ? launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
-                  : launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);
+    return geo == 1   ? launch<__half, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
+           : geo == 8 ? launch<__half, 8>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
+                      : launch<__half, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);
+  return geo == 1   ? launch<__nv_bfloat16, 1>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
+         : geo == 8 ? launch<__nv_bfloat16, 8>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s)
+                    : launch<__nv_bfloat16, 3>(ma, mb, mo, M, N, K, idesc, bn, group_m, ep, s);
 }
 
 }  // namespace krr

@@ -13,7 +13,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
     torch.manual_seed(0)
     out = {}
     s = torch.cuda.current_stream().cuda_stream
-    for (M, N, K) in [(65536 + 300, 768, 1024), (70000, 512, 4096)]:
+    for (M, N, K) in [(65536 + 300, 768, 1024), (70000, 512, 4096), (20000, 1024, 384),
+                      (17000, 256, 256)]:
         A = (torch.randn(M, K, device="cuda") * 0.5).half()
         B = (torch.randn(N, K, device="cuda") / math.sqrt(K)).half()
         for epi in (_lib.EPI_STORE, _lib.EPI_GELU, _lib.EPI_RESIDUAL):

@@ -182,6 +182,64 @@ def test_gemm_qkv_rope_scatter(backend):
     assert slabs[:, 1 - layer].abs().max().item() == 0
 
 
+@pytest.mark.parametrize("epi", [_lib.EPI_STORE, _lib.EPI_GELU, _lib.EPI_RESIDUAL])
+def test_gemm_pair_geometry_bit_identical(epi):
+    """Launches of 16k-131k rows run the CTA-pair geometry (G=8: cta_group::2,
+    256 rows per SM, accumulator halves handed over separately); smaller ones the
+    cluster-multicast G=3.  Same per-element MMA sequence: the rows of a ragged
+    M=16,684 launch equal the same rows computed by small launches bit for bit,
+    and match fp32 torch."""
+    M, N, K = 16384 + 300, 768, 1024
+    A = (torch.randn(M, K, device="cuda") * 0.5).half()
+    B = (torch.randn(N, K, device="cuda") / math.sqrt(K)).half()
+    if epi == _lib.EPI_RESIDUAL:
+        x0 = torch.randn(M, N, device="cuda")
+        full = x0.clone()
+    else:
+        full = torch.empty(M, N, dtype=torch.float16, device="cuda")
+    _gemm(_lib.GEMM_TCGEN05, _lib.F16, A, B, epi, full)
+    for r0, m in ((0, 4096), (M - 3000, 3000), (9000, 511)):
+        part = x0[r0:r0 + m].clone() if epi == _lib.EPI_RESIDUAL else \
+            torch.empty(m, N, dtype=torch.float16, device="cuda")
+        _gemm(_lib.GEMM_TCGEN05, _lib.F16, A[r0:r0 + m].contiguous(), B, epi, part)
+        torch.cuda.synchronize()
+        assert torch.equal(full[r0:r0 + m], part), (r0, m)
+    ref = A.float() @ B.float().T
+    if epi == _lib.EPI_GELU:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    if epi == _lib.EPI_RESIDUAL:
+        ref = x0 + ref
+    assert (full.float() - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
+
+
+def test_gemm_pair_geometry_qkv_scatter():
+    """The QKV RoPE scatter through the pair geometry (400 sequences x 48 rows =
+    19,200 rows) equals the same sequences scattered by two small launches."""
+    from paper_2504_02921_b200.model import rope_tables
+    H, KVH, HD, T, nseq, L, layer = 8, 2, 128, 48, 400, 2, 1
+    d, G, N = H * HD, H // KVH, (H + 2 * KVH) * HD
+    cos, sin = rope_tables(10000.0, HD, 1024)
+    cos_t, sin_t = torch.from_numpy(cos).cuda(), torch.from_numpy(sin).cuda()
+    A = torch.randn(nseq * T, d, device="cuda").half()
+    B = (torch.randn(N, d, device="cuda") / 16).half()
+
+    def run(a, n):
+        q_out = torch.zeros(n * KVH * G * T * HD, dtype=torch.float16, device="cuda")
+        slabs = torch.zeros(n, L, 2, KVH, T, HD, dtype=torch.float16, device="cuda")
+        ptrs = torch.arange(n, device="cuda", dtype=torch.int64) * (slabs[0].numel() * 2) + \
+            slabs.data_ptr()
+        qkv = _lib.QKV(H, KVH, HD, T, 512, layer, T, cos_t.data_ptr(), sin_t.data_ptr(),
+                       q_out.data_ptr(), ptrs.data_ptr())
+        _gemm(_lib.GEMM_TCGEN05, _lib.F16, a.contiguous(), B, _lib.EPI_QKV_ROPE, None, qkv)
+        torch.cuda.synchronize()
+        return q_out.view(n, -1), slabs
+    q_full, s_full = run(A, nseq)
+    h = nseq // 2
+    for i0 in (0, h):
+        q_p, s_p = run(A[i0 * T:(i0 + h) * T], h)
+        assert torch.equal(q_full[i0:i0 + h], q_p) and torch.equal(s_full[i0:i0 + h], s_p)
+
+
 def _attn_ref(q, kp, vp, vlen, kc, vc, tv, G, T):
     """fp32 torch restatement of model.py:373-394 for one (seq, kv head)."""
     P = kp.shape[0]

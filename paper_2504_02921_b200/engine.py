@@ -26,6 +26,8 @@ DEFAULT_WORKSPACE_BUDGET = 32 << 30  # bytes of activations per krr_forward call
 # streaming is ~7 ms per pass-boundary against a 3.1 s step;
 # profiles/r02_chunk_ab.txt).
 SCORE_ROWS_PER_PASS = 32768
+# Document rows per prefill pass (same reasoning; 64 documents of 512 tokens)
+PREFILL_ROWS_PER_PASS = 32768
 
 # The reference calls score_* from several rerank worker threads at once
 # (pipeline.py:375-379, 488-504).  Device scratch (workspace,
@@ -149,7 +151,7 @@ def _prefill_slots(w, pool, slots, doc_tokens, valid_len, max_rows):
     slots_t = (slots if isinstance(slots, torch.Tensor) else
                to_device(np.asarray(slots, dtype=np.int64), dev)).to(dev).to(torch.int64)
     ptrs = pool.slot_ptrs(slots_t)
-    step = max(1, (max_rows or rows_budget(w)) // D)
+    step = max(1, (max_rows or min(rows_budget(w), PREFILL_ROWS_PER_PASS)) // D)
     for i in range(0, n, step):
         j = min(n, i + step)
         run_forward(w, tok[i:j].contiguous(), valid[i:j].contiguous(), 0, 0, None, None,

@@ -665,7 +665,7 @@ def run_ours(args, rank, world, local_rank):
                          "class_split_pass": "second pass of the same K steps with CUDA events "
                                              "around every launch (krr_profile_*)",
                          "pairs_roofline": roof_pps, "pairs_frac": value / world / roof_pps,
-                         "traffic_launch": "MLP-up GEMM (ncu, profiles/traffic_c3.json)",
+                         "traffic_launch": "MLP-up GEMM of one 32k-row scoring pass (ncu, profiles/traffic_c3.json)",
                          "traffic_algorithmic": traffic_alg,
                          "attention": {
                              "bound": "tensor" if attn_tensor_bound else "hbm",

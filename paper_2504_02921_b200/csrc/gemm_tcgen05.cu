@@ -443,47 +443,35 @@ __global__ void __launch_bounds__(threads_of<G>(), 1)
         }
       }
     } else {
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    const uint64_t dA = sw128_desc(smem_u32(sA));
-    const uint64_t dB = sw128_desc(smem_u32(sB));
-    for (int tile = cid; tile < tiles; tile += ncl, ++it) {
-      const int acc = PAIR ? 0 : it & 1;
-      const uint32_t acc_phase = PAIR ? it & 1 : (it >> 1) & 1;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;   // accumulators 256 columns apart
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[stage], phase);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      const uint64_t dA = sw128_desc(smem_u32(sA));
+      const uint64_t dB = sw128_desc(smem_u32(sB));
+      for (int tile = cid; tile < tiles; tile += ncl, ++it) {
+        const int acc = it & 1;                         // double-buffered accumulators
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (elect_one_sync()) {
+        const uint32_t d_tmem = tmem_base + acc * BN;   // 256 columns apart
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            if constexpr (PAIR) {
-              mma_f16<2>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
-                         dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
-              mma_f16<2>(d_tmem + BN, dA + ((stage * A_BYTES + 128 * 128 + k * 32) >> 4),
-                         dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
-            } else {
+            for (int k = 0; k < BK / 16; ++k)
               mma_f16<1>(d_tmem, dA + ((stage * A_BYTES + k * 32) >> 4),
                          dB + ((stage * B_BYTES + k * 32) >> 4), idesc, (kb | k) != 0);
-            }
+            // completion frees the stage in every CTA that holds its operands
+            if constexpr (G == 1) mma_commit<1>(&empty[stage]);
+            else mma_commit_mc1(&empty[stage], (uint16_t)0x3);
           }
-          // completion frees the stage in every CTA that holds its operands
-          if constexpr (G == 1) mma_commit<1>(&empty[stage]);
-          else if constexpr (PAIR) mma_commit<2>(&empty[stage]);
-          else mma_commit_mc1(&empty[stage], (uint16_t)0x3);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (elect_one_sync()) mma_commit<1>(&tfull[acc]);
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (elect_one_sync()) {
-        if constexpr (PAIR) mma_commit<2>(&tfull[acc]);
-        else mma_commit<1>(&tfull[acc]);
-      }
-      __syncwarp();
-    }
     }
   } else {
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access

@@ -1,8 +1,8 @@
 // Persistent ping-pong tensor-core attention with P kept in TMEM (sm_100a).
 //
 // Same semantics as attention.cu (model.py:349-394, _exp_rows :406-436).
-// Relative to attention_pp.cu this kernel removes the shared-memory traffic
-// that bounded it (MMA operand reads of P, the softmax's P stores):
+// Relative to round 1's smem-P ping-pong kernel (removed) it keeps P out of
+// shared memory (no MMA operand reads of P, no softmax P stores there):
 //
 //  * P (16-bit) is written by the softmax warps straight back into the TMEM
 //    columns that held S (tcgen05.st) and consumed as the TMEM A operand of

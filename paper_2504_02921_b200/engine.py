@@ -25,7 +25,7 @@ DEFAULT_WORKSPACE_BUDGET = 32 << 30  # bytes of activations per krr_forward call
 # than one 307k-row pass (the power-capped clock is higher; the extra weight
 # streaming is ~7 ms per pass-boundary against a 3.1 s step;
 # profiles/r02_chunk_ab.txt).
-SCORE_ROWS_PER_PASS = 32768
+SCORE_ROWS_PER_PASS = 32768   # cap; passes are balanced (_balanced_step)
 # Document rows per prefill pass (same reasoning; 64 documents of 512 tokens)
 PREFILL_ROWS_PER_PASS = 32768
 
@@ -139,6 +139,14 @@ def prefill_slots(w: DeviceWeights, pool: KVPool, slots, doc_tokens, valid_len,
         _prefill_slots(w, pool, slots, doc_tokens, valid_len, max_rows)
 
 
+def _balanced_step(n: int, cap: int) -> int:
+    """Pass size for n units with at most cap per pass, spread evenly over the
+    minimum number of passes (C3: 10 passes of 640 pairs rather than 9 of 682 plus
+    a 262-pair tail that would fall below the CTA-pair GEMM geometry's 16k rows)."""
+    passes = -(-n // cap) if n > 0 else 1
+    return max(1, -(-n // passes))
+
+
 def _prefill_slots(w, pool, slots, doc_tokens, valid_len, max_rows):
     import torch
     if pool.code != w.code:
@@ -151,7 +159,7 @@ def _prefill_slots(w, pool, slots, doc_tokens, valid_len, max_rows):
     slots_t = (slots if isinstance(slots, torch.Tensor) else
                to_device(np.asarray(slots, dtype=np.int64), dev)).to(dev).to(torch.int64)
     ptrs = pool.slot_ptrs(slots_t)
-    step = max(1, (max_rows or min(rows_budget(w), PREFILL_ROWS_PER_PASS)) // D)
+    step = _balanced_step(n, max(1, (max_rows or min(rows_budget(w), PREFILL_ROWS_PER_PASS)) // D))
     for i in range(0, n, step):
         j = min(n, i + step)
         run_forward(w, tok[i:j].contiguous(), valid[i:j].contiguous(), 0, 0, None, None,
@@ -234,7 +242,7 @@ def _score_slots(w, pool, slots, q_tokens, q_valid, last_index, max_rows, out, w
         final, scores = scores, torch.empty(n, dtype=torch.float32, device=dev)
     prefix_ptrs = pool.slot_ptrs(slots_t)
     prefix_valid = pool.valid_len[slots_t]
-    step = max(1, (max_rows or min(rows_budget(w), SCORE_ROWS_PER_PASS)) // Q)
+    step = _balanced_step(n, max(1, (max_rows or min(rows_budget(w), SCORE_ROWS_PER_PASS)) // Q))
     scratch = scratch or _SCRATCH.setdefault(str(dev), SuffixScratch())
     D = pool.document_len
     for i in range(0, n, step):

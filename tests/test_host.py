@@ -199,3 +199,17 @@ def test_bench_work_accounting():
     gemm = 2 * L * Q * (d * (H + 2 * KVH) * HD + H * HD * d + 2 * d * 4 * d)
     assert f - a == gemm
     assert bench.kv_bytes_per_pair(cfg, D) == 2 * L * KVH * D * HD * 2 == 67108864
+
+
+def test_balanced_pass_split():
+    """Scoring/prefill passes: the fewest passes of <= cap units, sized evenly
+    (C3: 6,400 pairs at 682 per pass -> 10 passes of 640, not 9 + a 262 tail)."""
+    from paper_2504_02921_b200.engine import _balanced_step
+    assert _balanced_step(6400, 682) == 640
+    assert _balanced_step(100, 682) == 100
+    assert _balanced_step(1, 1) == 1
+    assert _balanced_step(0, 5) == 1
+    for n in (1, 7, 683, 1364, 1365, 6400):
+        for cap in (1, 3, 64, 682):
+            s = _balanced_step(n, cap)
+            assert s <= cap and -(-n // s) == -(-n // cap)

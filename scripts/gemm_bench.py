@@ -1,6 +1,6 @@
 """Micro-benchmark of the tcgen05 GEMM on the C3 (7B) shapes, per epilogue.
 
-    KRR_GEMM_CTA=1|2 python scripts/gemm_bench.py [--m 65536] [--reps 20]
+    python scripts/gemm_bench.py [--m 65536] [--reps 20]   (KRR_LIB=<variant .so> to A/B a variant library)
 
 Prints TF/s per shape plus SM clock / power sampled during the loop, and
 torch.matmul (cuBLAS) on the same shape for reference.
@@ -48,7 +48,7 @@ def main():
               ("up_store", 4 * d, d, _lib.EPI_STORE)]
     L = _lib.lib()
     s = torch.cuda.current_stream().cuda_stream
-    res = {"cta": os.environ.get("KRR_GEMM_CTA", "default"), "M": M}
+    res = {"lib": os.environ.get("KRR_LIB", "default"), "M": M}
     for name, N, K, epi in shapes:
         A = (torch.randn(M, K, device="cuda") * 0.5).half()
         B = (torch.randn(N, K, device="cuda") * 0.02).half()

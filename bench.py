@@ -640,7 +640,7 @@ def run_ours(args, rank, world, local_rank):
         attn_tf = attn_flops / attn_s / 1e12 if attn_s else 0
         attn_tensor_bound = attn_flops / (peak_s * 1e12) >= attn_bytes / (hbm * 1e9)
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:    # the CPU leg: rank 0 at N=1 only
             v, info = cpu_pairs_per_s(preset, D, Q)
             cpu = {"value": v, "unit": "pairs/s", **info}
         step_ms = ms / args.steps

@@ -510,6 +510,31 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     barrier()
+    # latency-sized steps (C2: 4,800 suffix rows) are launch-gap-bound when issued
+    # eagerly: time them as one CUDA-graph replay of the scoring pass + top-k
+    # (engine.GraphedScorer, device-resident inputs); at N=1 all pairs are local,
+    # so the graph's per-query top-k over doc ids is the step's selection
+    use_graph = args.graph == "on" or (
+        args.graph == "auto" and world == 1 and n_local * Q <= pipeline.GRAPH_MAX_ROWS)
+    timed_step, graph_launches = step, 0
+    if use_graph:
+        if world != 1:
+            raise SystemExit("--graph on needs N=1 (the graph has no all-gather)")
+        gsc = engine.GraphedScorer(w, pool, nq, nc, Q, k)
+        graph_launches = gsc.launches
+        q_all = q_dev.index_select(0, torch.arange(nq, device=dev)).contiguous()
+
+        def timed_step():
+            return gsc.replay_device(slots_dev, q_all, gid_dev)
+        # the replay must select the same (doc id, score) lists as the eager step
+        gi, gsc_s = timed_step()
+        gdoc = gid_dev.view(nq, nc).gather(1, gi.long())
+        ei, es = step()
+        if not (torch.equal(gdoc, ei) and torch.equal(gsc_s, es)):
+            raise SystemExit("graph replay and eager step disagree")
+        for _ in range(args.warmup):
+            timed_step()
+        barrier()
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n_launch0 = _lib.launch_count()
@@ -517,11 +542,11 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.nvtx.range_push("timed")
         e0.record(stream)
         for _ in range(args.steps):
-            step()
+            timed_step()
         e1.record(stream)
         torch.cuda.nvtx.range_pop()
         barrier()
-    launches = _lib.launch_count() - n_launch0
+    launches = _lib.launch_count() - n_launch0 + graph_launches * args.steps * use_graph
     ms = e0.elapsed_time(e1)
     # per-kernel-class device time (CUDA events around every launch, krr_profile_*)
     # from a second pass of the same K steps: the per-launch events cost host time
@@ -651,7 +676,10 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic (reference random-init weights, seed 0; "
                                               "uniform token ids)",
-            "config": workload_config(args, cfg, lay, corpus, nq, nc, keep, world),
+            "config": {**workload_config(args, cfg, lay, corpus, nq, nc, keep, world),
+                       "timed_step": ("one CUDA-graph replay (engine.GraphedScorer: scoring "
+                                      "pass + per-query top-k, device-resident inputs)"
+                                      if use_graph else "eager launches")},
             "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "paper_2504_02921_b200.pipeline.rerank"},
             "gpu_launches": int(launches),
@@ -744,6 +772,9 @@ def main():
     ap.add_argument("--latency-reps", type=int, default=20)
     ap.add_argument("--full-pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="time the scoring step as one CUDA-graph replay (auto: N=1 and "
+                         "latency-sized steps, <= pipeline.GRAPH_MAX_ROWS suffix rows)")
     ap.add_argument("--max-rows", type=int, default=0,
                     help="suffix rows per forward pass (0 = as many as the workspace budget allows)")
     ap.add_argument("--query-lens", default="", help="C5 sweep, e.g. 16,32,48,64,128,256")

@@ -451,8 +451,10 @@ class GraphedScorer:
         torch.cuda.current_stream(dev).wait_stream(self.stream)
         torch.cuda.synchronize(dev)
         self.graph = torch.cuda.CUDAGraph()
+        n0 = _lib.launch_count()
         with torch.cuda.graph(self.graph, stream=self.stream):
             self.out_idx, self.out_sc = self._body()
+        self.launches = _lib.launch_count() - n0      # this library's kernels per replay
         self._generation = self.pool.generation
         self._slab_ptr = self.pool.slab.data_ptr()
 
@@ -461,6 +463,22 @@ class GraphedScorer:
                     out=self.scores, max_rows=self.n_q * self.n_c * self.Q, ws=self._ws,
                     scratch=self._scratch)
         return segmented_topk(self.scores, self.ids, self.n_q, self.n_c, self.k)
+
+    def replay_device(self, slots, q_tokens, doc_ids):
+        """Device-resident variant of ``__call__``: slots int64 [n_q*n_c], q_tokens
+        int32 [n_q, Q], doc_ids int32 [n_q*n_c] already on the device are copied
+        into the static buffers on the current stream; returns the device
+        (idx, scores) [n_q, k] the replay writes (valid until the next replay)."""
+        import torch
+        with device_lock(self.w.device):
+            if (self.pool.generation != self._generation or
+                    self.pool.slab.data_ptr() != self._slab_ptr):
+                self._capture()
+            self.slots.copy_(slots)
+            self.q.copy_(q_tokens)
+            self.ids.copy_(doc_ids)
+            self.graph.replay()
+            return self.out_idx, self.out_sc
 
     def __call__(self, slots, q_tokens, doc_ids):
         """slots int [n_q*n_c], q_tokens int [n_q, Q], doc_ids int [n_q*n_c] (host);

@@ -377,3 +377,26 @@ def test_graphed_scorer_matches_eager(model16):
             order = sorted(range(6), key=lambda j: (-seg[j], perm[qi, j]))[:3]
             assert idx[qi].tolist() == order
             assert np.array_equal(sc[qi], seg[order])
+
+
+def test_graphed_scorer_replay_device_matches_host_call(model16):
+    """replay_device (device-resident inputs, bench's latency-sized timed step)
+    returns the same top-k as the host-buffer call and counts its launches."""
+    import torch
+    rng = np.random.default_rng(11)
+    docs = rng.integers(1, 32768, (6, 128))
+    pool = krr.KVPool(C1[0], 128, 6, "f16")
+    slots = pool.allocate([f"d{i}" for i in range(6)])
+    engine.prefill_slots(model16.weights, pool, slots, docs, np.full(6, 128))
+    gs = engine.GraphedScorer(model16.weights, pool, 2, 6, 48, 3)
+    assert gs.launches > 0
+    q = rng.integers(1, 32768, (2, 48))
+    perm = np.stack([rng.permutation(6) for _ in range(2)])
+    sl = slots[perm].reshape(-1)
+    idx_h, sc_h = gs(sl, q, perm.reshape(-1))
+    dev = model16.weights.device
+    idx_d, sc_d = gs.replay_device(torch.as_tensor(sl, device=dev),
+                                   torch.as_tensor(q.astype(np.int32), device=dev),
+                                   torch.as_tensor(perm.reshape(-1).astype(np.int32), device=dev))
+    assert np.array_equal(idx_d.cpu().numpy(), idx_h)
+    assert np.array_equal(sc_d.cpu().numpy(), sc_h)
